@@ -1,0 +1,350 @@
+"""Benchmark: full RQA of the N = 2^20 uniform series (config C3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C3] [--no-cpu-baseline]
+
+One step = one complete analysis of the configured workload: the recurrence
+test over all N^2 cells, diagonal / vertical / white-vertical line
+extraction, cross-band (and, for N > 1 GPUs, cross-stripe) stitching and the
+histogram reduction.  ``value`` is whole-job recurrence cells per second
+with the series resident in HBM (CUDA events on the launching stream, max
+over ranks); ``e2e`` is the same metric through the public API with the
+host series copied in and the histograms copied out every step.
+``--impl reference`` times the CPU restatement of the reference algorithm
+(oracle/, all host threads) on a bounded prefix sample of the same workload.
+Prints one JSON line on rank 0.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "recurrence cells/sec & full-RQA wall time, N=2^20, at 1/2/4/8 B200 vs CPU ref"
+UNIT = "cells/s"
+
+
+def ops_per_cell(settings) -> int:
+    """Algorithmic FP64 ops per cell of the reference formulation."""
+    m = settings.embedding_dimension
+    if m == 1:
+        return 2
+    return 3 * m if settings.metric == "l2" else 2 * m
+
+
+def executed_ops_per_cell(settings) -> int:
+    """FP64 ops per cell the reuse kernel actually issues (term reuse, App. A.3/A.4)."""
+    m = settings.embedding_dimension
+    if m == 1 or settings.metric == "linf":
+        return 2
+    return m + 2 if settings.metric == "l2" else m + 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(f) == 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_reference(settings, series_full, n_full, budget_s=20.0, threads=None):
+    """Time the oracle port (CPU restatement of tiledrqa) on a prefix sample.
+
+    Grows the prefix until one run takes >= budget_s/4, then reports the
+    cells/s of the largest run (bounded to ~budget_s of CPU work overall).
+    """
+    from oracle.oracle import oracle_histograms
+
+    threads = threads or len(os.sched_getaffinity(0))
+    m, tau = settings.embedding_dimension, settings.time_delay
+    span = (m - 1) * tau
+    n = 4096
+    best = None
+    spent = 0.0
+    while True:
+        n = min(n, n_full)
+        s = series_full[: n + span]
+        t0 = time.perf_counter()
+        oracle_histograms(s, m, tau, settings.metric, settings.radius, settings.theiler_window,
+                          tile_size=1024, workers=threads)
+        dt = time.perf_counter() - t0
+        spent += dt
+        best = (n, dt)
+        if dt >= budget_s / 4 or n >= n_full or spent + 4.5 * dt > budget_s:
+            break
+        n *= 2
+    n, dt = best
+    return {"value": n * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"prefix of {n} vectors ({n * n:.3e} cells) of the same series, "
+                      f"{dt:.2f} s, oracle/rqa_oracle.c tiled port, tile 1024"}
+
+
+def flush_l2(buf):
+    buf.add_(1)  # 256 MiB write > 126 MB L2
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+
+    from paper_2402_16853_b200.workloads import WORKLOADS, series_sha256
+
+    wl = WORKLOADS[args.workload]
+    settings = wl.settings
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": f"{wl.name}: {wl.description}", "n_vectors": wl.n_vectors(),
+              "m": settings.embedding_dimension, "tau": settings.time_delay,
+              "metric": settings.metric, "radius": settings.radius,
+              "theiler": settings.theiler_window, "parallelism": f"row stripes x{args.gpus}",
+              "l2_between_steps": "flushed (256 MiB write) before every timed step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        series = wl.series()
+        n_full = wl.n_vectors()
+        per_step = []
+        info = None
+        for i in range(args.warmup + args.steps):
+            info = cpu_reference(settings, series, n_full,
+                                 budget_s=max(4.0, 60.0 / (args.warmup + args.steps)))
+            if i >= args.warmup:
+                per_step.append(info["value"])
+        val = float(np.median(per_step))
+        out = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference",
+               "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": 1e3 * (wl.n_vectors() ** 2) / val, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded, sha256 " + series_sha256(series)[:16] + ")",
+               "config": config,
+               "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"],
+                                "kind": "port", "sample": info["sample"]},
+               "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0},
+               "note": "ms_per_step is the N^2-extrapolated wall of the full workload"}
+        print(json.dumps(out))
+        return
+
+    import torch
+
+    from paper_2402_16853_b200 import _native, embed, run_analysis
+    from paper_2402_16853_b200.device import MODE_FINAL, MODE_STRIPE, band_rows, run_rows_device
+    from paper_2402_16853_b200.distributed import stripe_bounds
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lib = _native.lib()
+    series_np = wl.series()
+    n = wl.n_vectors()
+    series = torch.from_numpy(series_np).to(dev)
+    hist = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
+    points = torch.zeros(1, dtype=torch.int64, device=dev)
+    pre = torch.zeros(n, dtype=torch.int32, device=dev)
+    suf = torch.zeros(n, dtype=torch.int32, device=dev)
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    bounds = stripe_bounds(n, world, band_rows(settings))
+    lo, hi = bounds[rank], bounds[rank + 1]
+    if world > 1:
+        pre_all = torch.empty(world, n, dtype=torch.int32, device=dev)
+        suf_all = torch.empty(world, n, dtype=torch.int32, device=dev)
+
+    def step():
+        hist.zero_()
+        points.zero_()
+        if world == 1:
+            run_rows_device(series, settings, 0, n, MODE_FINAL, hist, points, stream=stream)
+        else:
+            run_rows_device(series, settings, lo, hi, MODE_STRIPE, hist, points, pre, suf,
+                            stream=stream)
+            dist.all_gather_into_tensor(pre_all, pre)
+            dist.all_gather_into_tensor(suf_all, suf)
+            dist.reduce(hist, dst=0)
+            dist.reduce(points, dst=0)
+            if rank == 0:
+                from paper_2402_16853_b200.device import stitch_device
+
+                stitch_device(pre_all, suf_all, bounds, n, hist)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # kernel-level timing of the dominant (band) kernel: one isolated launch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    times = []
+    launches0 = lib.rqa_launch_counter()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            barrier()
+            ev[0].record(stream)
+            step()
+            ev[1].record(stream)
+            barrier()
+            times.append(ev[0].elapsed_time(ev[1]) * 1e-3)
+    launches = lib.rqa_launch_counter() - launches0
+    t_step = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    cells = float(n) * float(n)
+    value = cells / t_step
+
+    # band kernel alone (no fold) on this rank for the roofline
+    hist.zero_()
+    points.zero_()
+    barrier()
+    kern_times = []
+    for _ in range(3):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        run_rows_device(series, settings, lo, hi, MODE_FINAL if world == 1 else MODE_STRIPE,
+                        hist, points, pre, suf, stream=stream)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        kern_times.append(ev[0].elapsed_time(ev[1]) * 1e-3)
+    t_kern = float(np.min(kern_times))
+
+    # e2e through the public API: host series in, histograms out, every step
+    e2e_val = None
+    h2d = series_np.nbytes
+    d2h = 3 * (n + 1) * 8 + 8
+    if world == 1:
+        emb = embed(series_np, settings.embedding_dimension, settings.time_delay)
+        run_analysis(emb, settings)
+        e2e_t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            run_analysis(emb, settings)
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_val = cells / float(np.mean(e2e_t))
+    else:
+        from paper_2402_16853_b200.distributed import run_analysis_distributed
+
+        emb = embed(series_np, settings.embedding_dimension, settings.time_delay)
+        run_analysis_distributed(emb, settings, device=dev)
+        barrier()
+        t0 = time.perf_counter()
+        run_analysis_distributed(emb, settings, device=dev)
+        barrier()
+        e2e_val = cells / (time.perf_counter() - t0)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    dadd = ctypes.c_double()
+    dmul = ctypes.c_double()
+    err = ctypes.create_string_buffer(256)
+    lib.rqa_fp64_peak(local, ctypes.byref(dadd), ctypes.byref(dmul), err, 256)
+    peak = min(dadd.value, dmul.value)
+    local_cells = float(hi - lo) * float(n)
+    alg_ops = local_cells * ops_per_cell(settings)
+    achieved = alg_ops / t_kern
+    roofline = {
+        "bound": "fp64", "unit": "FP64 op/s",
+        "achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
+        "peak_source": "measured in-run: rqa_fp64_peak DADD/DMUL microbenchmark (not in "
+                       "MEASURED_PEAKS.json, which has only HBM and bf16)",
+        "traffic": None,
+        "kernel": "band_kernel (fused test + runs + histograms) + fold, one launch pair",
+        "kernel_s": t_kern,
+        "algorithmic_ops_per_cell": ops_per_cell(settings),
+        "executed_fp64_ops_per_cell": executed_ops_per_cell(settings),
+        "executed_frac": local_cells * executed_ops_per_cell(settings) / t_kern / peak
+        if peak else None,
+    }
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, sha256 " + series_sha256(series_np)[:16] + ")",
+           "config": config,
+           "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h},
+           "gpu_launches": int(launches),
+           "roofline": roofline,
+           "clocks": clocks.summary(),
+           "full_rqa_wall_s": cells / e2e_val if e2e_val else None}
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_reference(settings, series_np, n, budget_s=args.cpu_budget)
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,114 @@
+/*
+ * rqa_b200.h -- C-ABI of the B200-native RQA engine (librqa_b200.so).
+ *
+ * This boundary replaces the reference's tiled engine entry point
+ *     tiledrqa.engine.run_analysis(embedded, settings, tile_size, workers)
+ *     (/root/reference/pkg/src/tiledrqa/engine.py:215-280)
+ * which the reference's API calls from analyze() (__init__.py:31-39) and the
+ * CLI (cli.py:129-131).  The Python mirror paper_2402_16853_b200.engine
+ * .run_analysis binds these symbols with ctypes.
+ *
+ * Conventions: plain pointers and sizes only; series are float64 samples of
+ * the scalar time series (the embedding is implicit, embedding.py:32-69);
+ * histograms are int64[n+1] with index = line length (index 0 unused), like
+ * LineHistograms (histograms.py:16-67).  metric: 0 = L1 (manhattan),
+ * 1 = L2 (euclidean), 2 = Linf (maximum) (settings.py:9-23).  theiler: 0 keeps
+ * the main diagonal (reference default), 1 = include_main_diagonal=False
+ * (embedding.py:158-171), w > 1 zeroes every cell with |i-j| < w (extension).
+ *
+ * Return codes: 0 ok; RQA_EINVAL (-1) -> InvalidArgument;
+ * RQA_ESHORT (-2) -> SeriesTooShort (embedding.py:64-68); RQA_EDEVICE (-3)
+ * -> DeviceError (CUDA failure); RQA_ENOMEM (-4) -> DeviceError (allocation).
+ * A message is written to err (NUL-terminated, at most errlen bytes).
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point returns RQA_EDEVICE.
+ */
+#ifndef RQA_B200_H
+#define RQA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RQA_OK 0
+#define RQA_EINVAL (-1)
+#define RQA_ESHORT (-2)
+#define RQA_EDEVICE (-3)
+#define RQA_ENOMEM (-4)
+
+/* Number of timing slots written by rqa_run (seconds):
+ * [0] h2d, [1] band kernel, [2] fold kernel, [3] d2h, [4] total device span,
+ * [5] cells per second over the band+fold kernels, [6] band height,
+ * [7] number of bands. */
+#define RQA_TIMING_SLOTS 8
+
+/* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
+int rqa_version(void);
+
+/* Number of visible CUDA devices (0 when none / no driver). */
+int rqa_device_count(void);
+
+/* Total kernel launches issued by this library since load (for evidence of
+ * GPU execution in benchmarks). */
+int64_t rqa_launch_counter(void);
+
+/* Exact threshold used by the kernels: T* = max{x : RN(sqrt(x)) <= radius}
+ * for L2 with m > 1 (replaces sqrt, embedding.py:154-156), radius otherwise. */
+int rqa_threshold(int32_t metric, int32_t m, double radius, double *thr);
+
+/* Band height (rows per CTA) and kernel variant chosen for (metric, m, tau). */
+int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t *band_rows,
+                  int32_t *reuse_kernel);
+
+/*
+ * Full analysis of a host series on one device: replaces run_analysis
+ * (engine.py:215-280).  Writes the three histograms (int64[n+1] each, n =
+ * len - (m-1)*tau), the recurrence point count and RQA_TIMING_SLOTS timings.
+ */
+int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+            double radius, int64_t theiler, int32_t device, int64_t *diag, int64_t *vert,
+            int64_t *white, int64_t *points, double *timing, char *err, size_t errlen);
+
+/*
+ * Device-resident variant for callers that own device memory and a stream
+ * (torch tensors): rows [row_lo, row_hi) of the recurrence matrix.
+ *   mode 0 (final): rows must be [0, n); d_hist (int64[3*(n+1)], rows diag,
+ *     vert, white) and d_points are ACCUMULATED into (zero them first).
+ *   mode 1 (stripe): one row stripe of a multi-GPU run; diagonal runs that
+ *     touch the stripe's top/bottom edge are not counted but reported per
+ *     diagonal k >= 0 in d_stripe_prefix / d_stripe_suffix (int32[n]) for
+ *     rqa_stitch_device.  Vertical/white-vertical lines never cross stripes.
+ * stream is a cudaStream_t (NULL = legacy default stream); the call is
+ * asynchronous with respect to the host except for workspace growth.
+ */
+int rqa_run_device(const double *d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                   double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
+                   int64_t *d_hist, int64_t *d_points, int32_t *d_stripe_prefix,
+                   int32_t *d_stripe_suffix, void *stream, char *err, size_t errlen);
+
+/*
+ * Cross-stripe stitch (engine.py:287-319 carry contract + flush :195-212):
+ * d_prefix / d_suffix are int32[nstripes][n] gathered from every stripe in row
+ * order, bounds (host) the nstripes+1 stripe row boundaries.  Adds the
+ * diagonal runs that cross stripe edges into d_hist (diagonal row).
+ */
+int rqa_stitch_device(const int32_t *d_prefix, const int32_t *d_suffix, const int64_t *bounds,
+                      int32_t nstripes, int64_t n, int64_t *d_hist, void *stream, char *err,
+                      size_t errlen);
+
+/* FP64 pipe microbenchmark on `device`: sustained DADD and DMUL operations
+ * per second (the roofline denominator of the FP64-bound band kernel). */
+int rqa_fp64_peak(int32_t device, double *dadd_per_s, double *dmul_per_s, char *err,
+                  size_t errlen);
+
+/* Release cached device workspaces of this process. */
+int rqa_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RQA_B200_H */

@@ -1,0 +1,18 @@
+// Reuse-kernel instantiations for metric l2 (see rqa_band.cuh).
+#include "rqa_variants.cuh"
+
+namespace rqa {
+
+bool find_variant_l2(int m, int tau, Variant* out) {
+#define RQA_CASE(MM, TT)                                                   \
+  if (m == MM && tau == TT) {                                              \
+    *out = make_variant<kL2, MM, TT, 8, 4, 256>(0);                       \
+    return true;                                                           \
+  }
+  RQA_CASE(2, 1) RQA_CASE(2, 2) RQA_CASE(2, 3) RQA_CASE(3, 1) RQA_CASE(3, 2)
+  RQA_CASE(3, 3) RQA_CASE(4, 1) RQA_CASE(4, 2) RQA_CASE(5, 1)
+#undef RQA_CASE
+  return false;
+}
+
+}  // namespace rqa

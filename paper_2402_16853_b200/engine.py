@@ -1,0 +1,107 @@
+"""The drop-in boundary: run_analysis (mirror of tiledrqa engine.py:215-280).
+
+``run_analysis(embedded, settings, tile_size, workers)`` keeps the
+reference's signature, validation and return value ``(LineHistograms,
+timing)``.  The work runs in librqa_b200.so on a B200 (csrc/): one fused
+kernel evaluates the neighbourhood test, bit-packs rows with warp-level
+transposes and extracts diagonal, vertical and white-vertical runs with
+carries; a fold kernel stitches runs across band edges.  ``tile_size`` and
+``workers`` are validated exactly as before and, like in the reference,
+cannot change the integer result (engine.py:226-227); the device geometry is
+chosen by the library.
+"""
+
+import ctypes
+import os
+import time
+
+import numpy as np
+
+from . import _native
+from .embedding import EmbeddedSeries
+from .errors import InvalidArgument
+from .histograms import LineHistograms
+from .settings import METRIC_CODES, AnalysisSettings
+
+__all__ = ["DEFAULT_TILE_SIZE", "default_workers", "run_analysis", "device_count",
+           "exact_threshold"]
+
+DEFAULT_TILE_SIZE = 4096  # engine.py:44 (accepted, validated, geometry is device-chosen)
+
+
+def default_workers() -> int:
+    """engine.py:47-52: execution contexts when none are requested."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def device_count() -> int:
+    return int(_native.lib().rqa_device_count())
+
+
+def exact_threshold(metric: str, m: int, radius: float) -> float:
+    """The kernels' threshold: T* for L2 with m > 1 (sqrt-free, exact), else radius."""
+    out = ctypes.c_double()
+    rc = _native.lib().rqa_threshold(METRIC_CODES[metric], m, float(radius), ctypes.byref(out))
+    if rc != 0:
+        raise InvalidArgument("invalid threshold arguments")
+    return out.value
+
+
+def _series_array(embedded: EmbeddedSeries) -> np.ndarray:
+    return np.ascontiguousarray(embedded.values, dtype=np.float64)
+
+
+def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
+                 tile_size: int = DEFAULT_TILE_SIZE, workers: int | None = None, *,
+                 device: int = 0):
+    """Full analysis on one B200; returns (LineHistograms, timing dict).
+
+    timing keeps the reference keys (create_recurrence_matrix holds the fused
+    kernel time, the two detector phases are fused into it and report 0.0)
+    and adds h2d, fold, d2h, device_total, cells_per_second, band_rows,
+    bands.  Multi-GPU runs go through ``paper_2402_16853_b200.distributed``.
+    """
+    if workers is None:
+        workers = default_workers()
+    if workers < 1:
+        raise InvalidArgument("workers must be >= 1")  # engine.py:231-232
+    if tile_size < 1:
+        raise InvalidArgument("tile_size must be >= 1")  # engine.py:123-124
+    if (embedded.embedding_dimension != settings.embedding_dimension
+            or embedded.time_delay != settings.time_delay):
+        raise InvalidArgument("embedded series and settings disagree on m / tau")
+    started = time.perf_counter()
+    s = _series_array(embedded)
+    n = embedded.n_vectors
+    diag = np.zeros(n + 1, np.int64)
+    vert = np.zeros(n + 1, np.int64)
+    white = np.zeros(n + 1, np.int64)
+    pts = np.zeros(1, np.int64)
+    tim = np.zeros(_native.TIMING_SLOTS, np.float64)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    _native.call("rqa_run",
+                 s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0],
+                 settings.embedding_dimension, settings.time_delay,
+                 METRIC_CODES[settings.metric], float(settings.radius),
+                 settings.theiler_window, int(device),
+                 diag.ctypes.data_as(p64), vert.ctypes.data_as(p64),
+                 white.ctypes.data_as(p64), pts.ctypes.data_as(p64),
+                 tim.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    hist = LineHistograms(n, int(pts[0]), diag, vert, white)
+    timing = {
+        "create_recurrence_matrix": float(tim[1]),
+        "detect_diagonal_lines": 0.0,
+        "detect_vertical_lines": 0.0,
+        "h2d": float(tim[0]),
+        "fold": float(tim[2]),
+        "d2h": float(tim[3]),
+        "device_total": float(tim[4]),
+        "cells_per_second": float(tim[5]),
+        "band_rows": int(tim[6]),
+        "bands": int(tim[7]),
+        "total": time.perf_counter() - started,
+    }
+    return hist, timing

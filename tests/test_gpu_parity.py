@@ -1,0 +1,215 @@
+"""Parity of the CUDA path with the reference (through the C-ABI).
+
+Golden fixtures come from tiledrqa itself; larger random cases are checked
+against the C oracle (pinned to the reference by test_oracle_golden.py); at
+full benchmark size the checks are size-independent identities.  Integer
+results must be bit-identical.
+"""
+
+import numpy as np
+import pytest
+
+from fixtures import (assert_same, config_tags, load_cases, load_config, result_arrays,
+                      settings_obj, theiler_of)
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_available():
+    try:
+        from paper_2402_16853_b200 import _native
+
+        return _native.lib().rqa_device_count() > 0
+    except Exception:
+        return False
+
+
+if not _gpu_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2402_16853_b200 import (AnalysisSettings, compute_measures, embed,  # noqa: E402
+                                   run_analysis)
+
+
+def gpu_hist(series, settings):
+    e = embed(series, settings.embedding_dimension, settings.time_delay)
+    h, _ = run_analysis(e, settings)
+    return h.diagonal, h.vertical, h.white_vertical, h.recurrence_points
+
+
+def test_small_golden_cases():
+    fails = []
+    for series, st, res, meta in load_cases("small_cases"):
+        try:
+            assert_same(gpu_hist(series, settings_obj(st)), result_arrays(res), f"case {meta['id']}")
+        except AssertionError as exc:
+            fails.append(str(exc))
+    assert not fails, f"{len(fails)} failures: {fails[:5]}"
+
+
+def test_small_golden_measures():
+    for series, st, res, meta in load_cases("small_cases")[:60]:
+        s = settings_obj(st)
+        e = embed(series, s.embedding_dimension, s.time_delay)
+        h, _ = run_analysis(e, s)
+        got = compute_measures(h, s).measures_dict()
+        for k, v in meta["measures"].items():
+            if v is None:
+                assert got[k] is None, (meta["id"], k)
+            else:
+                assert got[k] == pytest.approx(v, rel=1e-12, abs=0), (meta["id"], k)
+
+
+def test_theiler_golden_cases():
+    for series, st, res, meta in load_cases("theiler_cases"):
+        assert_same(gpu_hist(series, settings_obj(st)), result_arrays(res),
+                    f"theiler case {meta['id']}")
+
+
+@pytest.mark.parametrize("tag", config_tags())
+def test_config_fixtures(tag):
+    from paper_2402_16853_b200.workloads import WORKLOADS, series_sha256
+
+    fx = load_config(tag)
+    wl = WORKLOADS[fx["workload"]]
+    series = wl.series(fx["samples"] if fx["prefix"] else None)
+    assert series_sha256(series) == fx["sha256"]
+    assert_same(gpu_hist(series, settings_obj(fx["settings"])), result_arrays(fx["result"]), tag)
+
+
+CASES = [
+    # (family, length, m, tau, metric, quantile, theiler)
+    ("uniform", 3000, 3, 1, "l2", 0.01, 0),
+    ("uniform", 4097, 3, 2, "linf", 0.02, 0),
+    ("sine", 5000, 2, 2, "l2", 0.4, 0),
+    ("sine", 2500, 1, 1, "l1", 0.05, 1),
+    ("ar1", 3333, 4, 1, "l1", 0.1, 1),
+    ("ar1", 2049, 5, 1, "linf", 0.3, 3),
+    ("uniform", 2111, 6, 3, "l2", 0.2, 0),      # direct (runtime m, tau) kernel
+    ("sine", 3001, 10, 5, "l1", 0.3, 10),       # C4 shape, direct kernel
+    ("uniform", 1800, 7, 1, "linf", 0.5, 2),    # direct Linf
+    ("sine", 6000, 2, 3, "l1", 0.9, 0),         # dense
+    ("uniform", 40, 3, 1, "l2", 1.0, 0),        # all ones
+    ("uniform", 33, 1, 1, "l2", 0.0, 0),        # only the main diagonal
+]
+
+
+def _series(family, length, rng):
+    if family == "uniform":
+        return rng.uniform(0, 1, length)
+    if family == "sine":
+        return np.sin(np.linspace(0, 40 * np.pi, length)) + 0.05 * rng.normal(size=length)
+    x = np.empty(length)
+    x[0] = 0.0
+    eps = rng.normal(size=length)
+    for i in range(1, length):
+        x[i] = 0.9 * x[i - 1] + 0.3 * eps[i]
+    return x
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-m{c[2]}t{c[3]}-{c[4]}" for c in CASES])
+def test_random_cases_vs_oracle(case, oracle_lib):
+    fam, length, m, tau, metric, q, w = case
+    rng = np.random.default_rng(length * 31 + m)
+    s = _series(fam, length, rng)
+    n = length - (m - 1) * tau
+    # radius from the quantile of sampled distances
+    from paper_2402_16853_b200 import distance
+
+    idx = rng.integers(0, n, (400, 2))
+    d = [distance(s[i: i + (m - 1) * tau + 1: tau], s[j: j + (m - 1) * tau + 1: tau], metric)
+         for i, j in idx]
+    radius = float(np.quantile(d, q)) if q > 0 else 0.0
+    st = AnalysisSettings(m, tau, metric, radius, theiler_corrector=w)
+    want = oracle_lib.oracle_histograms(s, m, tau, metric, radius, w, tile_size=512)
+    assert_same(gpu_hist(s, st), want, str(case))
+
+
+def test_nan_in_raw_array_matches_reference_semantics(oracle_lib):
+    """A raw ndarray is not finite-checked (embedding.py:59-60): NaN cells are 0."""
+    rng = np.random.default_rng(9)
+    s = rng.uniform(0, 1, 700)
+    s[[5, 300, 301, 650]] = np.nan
+    for metric in ("l1", "l2", "linf"):
+        for m, tau in ((1, 1), (3, 1), (2, 2), (6, 2)):
+            want = oracle_lib.oracle_histograms(s, m, tau, metric, 0.2, 0, tile_size=64)
+            assert_same(gpu_hist(s, AnalysisSettings(m, tau, metric, 0.2)), want,
+                        f"nan {metric} m{m} t{tau}")
+
+
+def test_spec_known_answers():
+    """SPEC.md examples: all-ones and identity-only matrices."""
+    for n in (3, 4, 7, 50, 1000):
+        s = np.zeros(n)
+        d, v, w, p = gpu_hist(s, AnalysisSettings(1, 1, "l2", 0.0))
+        assert p == n * n
+        want_d = np.zeros(n + 1, np.int64)
+        want_d[1:n] = 2
+        want_d[n] = 1
+        assert np.array_equal(d, want_d)
+        assert v[n] == n and v.sum() == n
+        assert w.sum() == 0
+    h = gpu_hist(np.arange(5.0), AnalysisSettings(1, 1, "l2", 0.5, include_main_diagonal=False))
+    assert h[3] == 0 and h[2][5] == 5 and h[2].sum() == 5
+    res = compute_measures(
+        run_analysis(embed(np.zeros(7), 1, 1), AnalysisSettings(1, 1, "l2", 0.0))[0],
+        AnalysisSettings(1, 1, "l2", 0.0))
+    assert res.det == pytest.approx(47 / 49) and res.l_max == 7 and res.lam == 1.0
+    assert res.tt == 7.0 and res.div == pytest.approx(1 / 7)
+
+
+def test_stripes_then_stitch_equal_single_run():
+    """Multi-GPU decomposition, emulated on one device: G stripes + stitch."""
+    import torch
+
+    from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, band_rows,
+                                              run_rows_device, stitch_device)
+    from paper_2402_16853_b200.distributed import stripe_bounds
+
+    rng = np.random.default_rng(11)
+    for metric, m, tau, r, length in (("l2", 3, 1, 0.12, 9000), ("linf", 2, 2, 0.3, 7001),
+                                      ("l1", 1, 1, 0.02, 5000)):
+        s = np.sin(np.linspace(0, 30 * np.pi, length)) + 0.2 * rng.uniform(-1, 1, length)
+        st = AnalysisSettings(m, tau, metric, r)
+        n = length - (m - 1) * tau
+        dev = torch.device("cuda", 0)
+        sd = torch.from_numpy(s).to(dev)
+        ref_h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
+        ref_p = torch.zeros(1, dtype=torch.int64, device=dev)
+        run_rows_device(sd, st, 0, n, MODE_FINAL, ref_h, ref_p)
+        band = band_rows(st)
+        for g in (1, 2, 3, 5):
+            bounds = stripe_bounds(n, g, band)
+            h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
+            p = torch.zeros(1, dtype=torch.int64, device=dev)
+            pre = torch.zeros(g, n, dtype=torch.int32, device=dev)
+            suf = torch.zeros(g, n, dtype=torch.int32, device=dev)
+            for q in range(g):
+                run_rows_device(sd, st, bounds[q], bounds[q + 1], MODE_STRIPE, h, p, pre[q], suf[q])
+            stitch_device(pre, suf, bounds, n, h)
+            torch.cuda.synchronize()
+            assert torch.equal(h, ref_h), (metric, g)
+            assert torch.equal(p, ref_p)
+
+
+def test_full_size_identities():
+    """C3 at full size (N = 2^20): conservation identities and symmetry-free checks."""
+    from paper_2402_16853_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS["C3"]
+    s = wl.series()
+    d, v, w, p = gpu_hist(s, wl.settings)
+    n = wl.n_vectors()
+    lengths = np.arange(n + 1, dtype=np.int64)
+    assert int((lengths * d).sum()) == p
+    assert int((lengths * v).sum()) == p
+    assert int((lengths * v).sum() + (lengths * w).sum()) == n * n
+    assert d[n] == 1                                      # main diagonal is one line
+    assert (d[1:n] % 2 == 0).all()                        # R = R^T pairs diagonals
+    # the prefix fixture is an exact sub-problem only for rows/cols < prefix;
+    # its recurrence rate must be close
+    fx = load_config("C3_65536") if "C3_65536" in config_tags() else None
+    if fx is not None:
+        rr_full = p / (n * n)
+        rr_pref = fx["result"]["recurrence_points"] / 65536 ** 2
+        assert abs(rr_full - rr_pref) < 2e-4

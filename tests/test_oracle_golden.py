@@ -1,0 +1,72 @@
+"""The CPU oracle (oracle/rqa_oracle.c) is pinned to the reference.
+
+Every golden fixture was produced by tiledrqa itself
+(tests/golden/make_golden.py); the oracle must reproduce each one exactly,
+at several tile sizes and worker counts (tiling/worker invariance,
+SPEC.md:239-240).
+"""
+
+import numpy as np
+import pytest
+
+from fixtures import assert_same, config_tags, load_cases, load_config, result_arrays, theiler_of
+
+SMALL = load_cases("small_cases")
+THEILER = load_cases("theiler_cases")
+
+
+def test_small_case_count():
+    assert len(SMALL) >= 200  # SPEC.md:465 acceptance criterion 1
+
+
+@pytest.mark.parametrize("tile,workers", [(1, 1), (7, 2), (64, 8), (100000, 3)])
+def test_oracle_small_cases(oracle_lib, tile, workers):
+    for series, st, res, meta in SMALL:
+        if tile == 1 and res["n_vectors"] > 120:
+            continue
+        got = oracle_lib.oracle_histograms(series, st["embedding_dimension"], st["time_delay"],
+                                           st["metric"], st["radius"], theiler_of(st),
+                                           tile_size=tile, workers=workers)
+        assert_same(got, result_arrays(res), f"case {meta['id']} tile {tile}")
+
+
+def test_oracle_theiler_cases(oracle_lib):
+    for series, st, res, meta in THEILER:
+        got = oracle_lib.oracle_histograms(series, st["embedding_dimension"], st["time_delay"],
+                                           st["metric"], st["radius"], theiler_of(st),
+                                           tile_size=37, workers=4)
+        assert_same(got, result_arrays(res), f"theiler case {meta['id']}")
+
+
+@pytest.mark.parametrize("tag", [t for t in config_tags() if t in ("C1", "C5_32768", "C4_16384",
+                                                                   "P_19999")])
+def test_oracle_config_fixtures(oracle_lib, tag):
+    from paper_2402_16853_b200.workloads import WORKLOADS, series_sha256
+
+    fx = load_config(tag)
+    wl = WORKLOADS[fx["workload"]]
+    series = wl.series(fx["samples"] if fx["prefix"] else None)
+    assert series_sha256(series) == fx["sha256"]
+    st = fx["settings"]
+    got = oracle_lib.oracle_histograms(series, st["embedding_dimension"], st["time_delay"],
+                                       st["metric"], st["radius"], theiler_of(st),
+                                       tile_size=1024)
+    assert_same(got, result_arrays(fx["result"]), tag)
+
+
+def test_oracle_matrix_symmetric_and_brute_force(oracle_lib):
+    """Bit level: R = R^T and agreement with scalar distances."""
+    from paper_2402_16853_b200 import distance
+
+    rng = np.random.default_rng(5)
+    for metric in ("l1", "l2", "linf"):
+        for m, tau in ((1, 1), (3, 2), (5, 1)):
+            s = rng.uniform(-3, 3, 70)
+            n = 70 - (m - 1) * tau
+            vec = [s[i: i + (m - 1) * tau + 1: tau] for i in range(n)]
+            r = float(np.median([distance(vec[0], v, metric) for v in vec]))
+            mat = oracle_lib.oracle_matrix(s, m, tau, metric, r)
+            assert np.array_equal(mat, mat.T)
+            brute = np.array([[distance(vec[i], vec[j], metric) <= r for j in range(n)]
+                              for i in range(n)])
+            assert np.array_equal(mat, brute)
