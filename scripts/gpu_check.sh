@@ -1,0 +1,6 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -20
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30
+timeout 600 python bench.py --steps 3 --warmup 3 --cpu-budget 10 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; tail -5 gpurun_out/bench1.err; cat gpurun_out/bench1.json

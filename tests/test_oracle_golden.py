@@ -38,8 +38,7 @@ def test_oracle_theiler_cases(oracle_lib):
         assert_same(got, result_arrays(res), f"theiler case {meta['id']}")
 
 
-@pytest.mark.parametrize("tag", [t for t in config_tags() if t in ("C1", "C5_32768", "C4_16384",
-                                                                   "P_19999")])
+@pytest.mark.parametrize("tag", config_tags())
 def test_oracle_config_fixtures(oracle_lib, tag):
     from paper_2402_16853_b200.workloads import WORKLOADS, series_sha256
 
