@@ -187,8 +187,9 @@ def main():
     import torch
 
     from paper_2402_16853_b200 import _native, embed, run_analysis
-    from paper_2402_16853_b200.device import MODE_FINAL, MODE_STRIPE, band_rows, run_rows_device
-    from paper_2402_16853_b200.distributed import stripe_bounds
+    from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, StripeOutputs, band_rows,
+                                              run_rows_device, stitch_device)
+    from paper_2402_16853_b200.distributed import exchange, stripe_bounds
 
     if world > 1:
         import torch.distributed as dist
@@ -203,15 +204,11 @@ def main():
     series = torch.from_numpy(series_np).to(dev)
     hist = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
     points = torch.zeros(1, dtype=torch.int64, device=dev)
-    pre = torch.zeros(n, dtype=torch.int32, device=dev)
-    suf = torch.zeros(n, dtype=torch.int32, device=dev)
+    so = StripeOutputs.empty(n, dev) if world > 1 else None
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     bounds = stripe_bounds(n, world, band_rows(settings))
     lo, hi = bounds[rank], bounds[rank + 1]
-    if world > 1:
-        pre_all = torch.empty(world, n, dtype=torch.int32, device=dev)
-        suf_all = torch.empty(world, n, dtype=torch.int32, device=dev)
 
     def step():
         hist.zero_()
@@ -219,16 +216,14 @@ def main():
         if world == 1:
             run_rows_device(series, settings, 0, n, MODE_FINAL, hist, points, stream=stream)
         else:
-            run_rows_device(series, settings, lo, hi, MODE_STRIPE, hist, points, pre, suf,
+            so.rowlead.zero_()
+            run_rows_device(series, settings, lo, hi, MODE_STRIPE, hist, points, so,
                             stream=stream)
-            dist.all_gather_into_tensor(pre_all, pre)
-            dist.all_gather_into_tensor(suf_all, suf)
+            gathered = exchange(so, world)
             dist.reduce(hist, dst=0)
             dist.reduce(points, dst=0)
             if rank == 0:
-                from paper_2402_16853_b200.device import stitch_device
-
-                stitch_device(pre_all, suf_all, bounds, n, hist)
+                stitch_device(gathered, bounds, n, hist)
 
     def barrier():
         if world > 1:
@@ -270,7 +265,7 @@ def main():
         torch.cuda.synchronize()
         ev[0].record(stream)
         run_rows_device(series, settings, lo, hi, MODE_FINAL if world == 1 else MODE_STRIPE,
-                        hist, points, pre, suf, stream=stream)
+                        hist, points, so, stream=stream)
         ev[1].record(stream)
         torch.cuda.synchronize()
         kern_times.append(ev[0].elapsed_time(ev[1]) * 1e-3)
@@ -312,7 +307,9 @@ def main():
     err = ctypes.create_string_buffer(256)
     lib.rqa_fp64_peak(local, ctypes.byref(dadd), ctypes.byref(dmul), err, 256)
     peak = min(dadd.value, dmul.value)
-    local_cells = float(hi - lo) * float(n)
+    # cells of the full matrix that this rank's stripe accounts for (upper
+    # triangle rows [lo, hi) stand for their mirrored lower-triangle cells too)
+    local_cells = float(n - lo + n - hi) * float(hi - lo)
     alg_ops = local_cells * ops_per_cell(settings)
     achieved = alg_ops / t_kern
     roofline = {

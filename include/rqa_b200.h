@@ -77,27 +77,39 @@ int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t m
  * (torch tensors): rows [row_lo, row_hi) of the recurrence matrix.
  *   mode 0 (final): rows must be [0, n); d_hist (int64[3*(n+1)], rows diag,
  *     vert, white) and d_points are ACCUMULATED into (zero them first).
- *   mode 1 (stripe): one row stripe of a multi-GPU run; diagonal runs that
- *     touch the stripe's top/bottom edge are not counted but reported per
- *     diagonal k >= 0 in d_stripe_prefix / d_stripe_suffix (int32[n]) for
- *     rqa_stitch_device.  Vertical/white-vertical lines never cross stripes.
+ *   mode 1 (stripe): one row stripe of a multi-GPU run.  Lines that cross
+ *     the stripe's edges are not counted; instead the stripe reports
+ *       d_stripe_prefix / d_stripe_suffix (int32[n]): per diagonal k >= 0 the
+ *         1-run starting at the stripe's top / ending at its bottom edge;
+ *       d_stripe_col (uint32[2n]): per column c the first and last run
+ *         ((len << 1) | bit) of the column's part inside the stripe above the
+ *         main diagonal;
+ *       d_rowlead (uint32[n], zero-initialised by the caller): for the
+ *         stripe's rows i, the first run of row i right of the diagonal.
+ *     All four go to rqa_stitch_device (after an all-gather / sum-reduce).
+ * Only the upper triangle k >= 0 is evaluated: R = R^T exactly, so diagonal
+ * -k equals diagonal k and column c equals the "hook" (upper column c above
+ * the diagonal, then upper row c) -- see DESIGN.md.
  * stream is a cudaStream_t (NULL = legacy default stream); the call is
  * asynchronous with respect to the host except for workspace growth.
  */
 int rqa_run_device(const double *d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                    double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
                    int64_t *d_hist, int64_t *d_points, int32_t *d_stripe_prefix,
-                   int32_t *d_stripe_suffix, void *stream, char *err, size_t errlen);
+                   int32_t *d_stripe_suffix, uint32_t *d_stripe_col, uint32_t *d_rowlead,
+                   void *stream, char *err, size_t errlen);
 
 /*
  * Cross-stripe stitch (engine.py:287-319 carry contract + flush :195-212):
- * d_prefix / d_suffix are int32[nstripes][n] gathered from every stripe in row
- * order, bounds (host) the nstripes+1 stripe row boundaries.  Adds the
- * diagonal runs that cross stripe edges into d_hist (diagonal row).
+ * d_prefix / d_suffix (int32[nstripes][n]) and d_col (uint32[nstripes][2n])
+ * gathered from every stripe in row order, d_rowlead (uint32[n]) summed over
+ * the stripes, bounds (host) the nstripes+1 stripe row boundaries.  Adds the
+ * diagonal, vertical and white-vertical lines that cross stripe edges into
+ * d_hist.
  */
-int rqa_stitch_device(const int32_t *d_prefix, const int32_t *d_suffix, const int64_t *bounds,
-                      int32_t nstripes, int64_t n, int64_t *d_hist, void *stream, char *err,
-                      size_t errlen);
+int rqa_stitch_device(const int32_t *d_prefix, const int32_t *d_suffix, const uint32_t *d_col,
+                      const uint32_t *d_rowlead, const int64_t *bounds, int32_t nstripes,
+                      int64_t n, int64_t *d_hist, void *stream, char *err, size_t errlen);
 
 /* FP64 pipe microbenchmark on `device`: sustained DADD and DMUL operations
  * per second (the roofline denominator of the FP64-bound band kernel). */

@@ -32,9 +32,9 @@ SYMBOLS = {
     "rqa_run": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _pi64, _pi64,
                            _pi64, _pi64, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_run_device": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _dbl, _i64, _i64, _i64, _i32,
-                                  _vp, _vp, _vp, _vp, _vp, _c.c_char_p, _c.c_size_t]),
-    "rqa_stitch_device": (_c.c_int, [_vp, _vp, _pi64, _i32, _i64, _vp, _vp, _c.c_char_p,
-                                     _c.c_size_t]),
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_char_p, _c.c_size_t]),
+    "rqa_stitch_device": (_c.c_int, [_vp, _vp, _vp, _vp, _pi64, _i32, _i64, _vp, _vp,
+                                     _c.c_char_p, _c.c_size_t]),
     "rqa_fp64_peak": (_c.c_int, [_i32, _pd, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_release": (_c.c_int, []),
 }

@@ -51,8 +51,12 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   double* s_pad = nullptr;
   size_t s_cap = 0;  // elements
-  uint16_t* ps = nullptr;
+  uint16_t* ps = nullptr;      // P and S (compact band layout)
   size_t ps_cap = 0;  // elements
+  uint32_t* cs = nullptr;      // column-part summaries (compact band layout)
+  size_t cs_cap = 0;
+  uint32_t* rowlead = nullptr; // [n]
+  size_t rowlead_cap = 0;
   unsigned long long* hist = nullptr;
   size_t hist_cap = 0;  // elements (3*(n+1) + 1 for points)
   int64_t* bounds = nullptr;
@@ -120,7 +124,7 @@ int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
                    (long long)span),
            RQA_EINVAL;
   const int64_t H = p->var.band_rows(), D = 32 * p->var.nw;
-  p->pad = H + 2 * D + p->var.hs + p->var.w + 256;
+  p->pad = 2 * H + 4 * D + p->var.w + 256;
   return RQA_OK;
 }
 
@@ -148,23 +152,24 @@ int stage_series(Workspace* ws, const Problem& p, const double* src, cudaMemcpyK
   return RQA_OK;
 }
 
-// Band kernel over rows [row_lo, row_hi) + fold (final or stripe).
+// Upper-triangle band kernel over rows [row_lo, row_hi) + folds.
+//   final mode: diagonal and hook folds write the complete histograms;
+//   stripe mode: per-stripe summaries for rqa_stitch_device (multi-GPU).
 int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi, int mode,
                 unsigned long long* hist, unsigned long long* points, int32_t* out_p,
-                int32_t* out_s, cudaStream_t st, cudaEvent_t ev_mid, char* err, size_t errlen) {
+                int32_t* out_s, uint32_t* out_col, uint32_t* rowlead, cudaStream_t st,
+                cudaEvent_t ev_mid, char* err, size_t errlen) {
   const int64_t H = p.var.band_rows();
   const int64_t nb = (row_hi - row_lo + H - 1) / H;
   if (nb <= 0) return RQA_OK;
-  const size_t ps_need = (size_t)(2 * nb) * (size_t)p.n;
-  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, ps_need), "allocating band summaries");
-  RQA_CUDA(grow(&ws->bounds, &ws->bounds_cap, (size_t)nb + 1), "allocating bounds");
-  std::vector<int64_t> b(nb + 1);
-  for (int64_t q = 0; q <= nb; ++q) b[q] = std::min(row_lo + q * H, row_hi);
-  RQA_CUDA(cudaMemcpyAsync(ws->bounds, b.data(), (nb + 1) * sizeof(int64_t),
-                           cudaMemcpyHostToDevice, st),
-           "copying bounds");
-
-  BandArgs a;
+  const int64_t total = sym_band_offset(nb, p.n, row_lo, H);  // compact entries
+  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * total)), "allocating band summaries");
+  RQA_CUDA(grow(&ws->cs, &ws->cs_cap, (size_t)total), "allocating column summaries");
+  if (!rowlead) {
+    RQA_CUDA(grow(&ws->rowlead, &ws->rowlead_cap, (size_t)p.n), "allocating row leads");
+    rowlead = ws->rowlead;
+  }
+  SymArgs a;
   a.s = ws->s_pad + p.pad;
   a.len = p.len;
   a.n = p.n;
@@ -175,28 +180,37 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.m = p.m;
   a.tau = p.tau;
   a.P = ws->ps;
-  a.S = ws->ps + (size_t)nb * p.n;
+  a.S = ws->ps + total;
+  a.colsum = ws->cs;
+  a.rowlead = rowlead;
   a.hist = hist;
   a.points = points;
   RQA_CUDA(p.var.launch(a, (int)nb, p.var.w, st), "launching band kernel");
   g_launches++;
   if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
 
-  FoldArgs<uint16_t> f;
+  SymFoldArgs f;
+  memset(&f, 0, sizeof f);
   f.P = a.P;
   f.S = a.S;
-  f.pitch = p.n;
-  f.bounds = ws->bounds;
-  f.nseg = (int)nb;
+  f.colsum = a.colsum;
+  f.row_lo = row_lo;
+  f.row_hi = row_hi;
+  f.H = H;
+  f.nb = (int)nb;
+  f.rowlead = rowlead;
   f.n = p.n;
   f.hist = hist;
   f.out_p = out_p;
   f.out_s = out_s;
+  f.out_col = reinterpret_cast<uint2*>(out_col);
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((p.n + threads - 1) / threads, 148 * 16);
-  fold_kernel<uint16_t><<<(int)blocks, threads, 0, st>>>(f, mode);
-  RQA_CUDA(cudaGetLastError(), "launching fold kernel");
-  g_launches++;
+  sym_fold_diag<<<(int)blocks, threads, 0, st>>>(f, mode);
+  RQA_CUDA(cudaGetLastError(), "launching diagonal fold");
+  sym_fold_hooks<<<(int)blocks, threads, 0, st>>>(f, mode);
+  RQA_CUDA(cudaGetLastError(), "launching hook fold");
+  g_launches += 2;
   return RQA_OK;
 }
 
@@ -280,8 +294,8 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
   if (rc) return rc;
   RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 1) * sizeof(unsigned long long), st), "memset");
   RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
-  rc = launch_rows(ws, p, 0, p.n, kFoldFinal, ws->hist, ws->hist + 3 * hn, nullptr, nullptr, st,
-                   ws->ev[2], err, errlen);
+  rc = launch_rows(ws, p, 0, p.n, kFoldFinal, ws->hist, ws->hist + 3 * hn, nullptr, nullptr,
+                   nullptr, nullptr, st, ws->ev[2], err, errlen);
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[3], st), "event");
   RQA_CUDA(cudaMemcpyAsync(diag, ws->hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
@@ -311,7 +325,8 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
 int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                    double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
                    int64_t* d_hist, int64_t* d_points, int32_t* d_stripe_prefix,
-                   int32_t* d_stripe_suffix, void* stream, char* err, size_t errlen) {
+                   int32_t* d_stripe_suffix, uint32_t* d_stripe_col, uint32_t* d_rowlead,
+                   void* stream, char* err, size_t errlen) {
   if (!d_series || !d_hist || !d_points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
   Problem p;
@@ -325,8 +340,9 @@ int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, 
            RQA_EINVAL;
   if (mode == kFoldFinal && (row_lo != 0 || row_hi != p.n))
     return set_err(err, errlen, "final mode needs the full row range"), RQA_EINVAL;
-  if (mode == kFoldStripe && (!d_stripe_prefix || !d_stripe_suffix))
-    return set_err(err, errlen, "stripe mode needs prefix/suffix outputs"), RQA_EINVAL;
+  if (mode == kFoldStripe && (!d_stripe_prefix || !d_stripe_suffix || !d_stripe_col || !d_rowlead))
+    return set_err(err, errlen, "stripe mode needs prefix/suffix/column/row-lead outputs"),
+           RQA_EINVAL;
   int dev = 0;
   RQA_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   Workspace* ws = workspace(dev);
@@ -338,13 +354,14 @@ int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, 
   (void)hn;
   return launch_rows(ws, p, row_lo, row_hi, mode, reinterpret_cast<unsigned long long*>(d_hist),
                      reinterpret_cast<unsigned long long*>(d_points), d_stripe_prefix,
-                     d_stripe_suffix, st, nullptr, err, errlen);
+                     d_stripe_suffix, mode == kFoldStripe ? d_stripe_col : nullptr,
+                     mode == kFoldStripe ? d_rowlead : nullptr, st, nullptr, err, errlen);
 }
 
-int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const int64_t* bounds,
-                      int32_t nstripes, int64_t n, int64_t* d_hist, void* stream, char* err,
-                      size_t errlen) {
-  if (!d_prefix || !d_suffix || !bounds || !d_hist || nstripes < 1 || n < 1)
+int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const uint32_t* d_col,
+                      const uint32_t* d_rowlead, const int64_t* bounds, int32_t nstripes, int64_t n,
+                      int64_t* d_hist, void* stream, char* err, size_t errlen) {
+  if (!d_prefix || !d_suffix || !d_col || !d_rowlead || !bounds || !d_hist || nstripes < 1 || n < 1)
     return set_err(err, errlen, "invalid stitch arguments"), RQA_EINVAL;
   if (bounds[0] != 0 || bounds[nstripes] != n)
     return set_err(err, errlen, "stripes must cover rows [0, n)"), RQA_EINVAL;
@@ -360,22 +377,21 @@ int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const in
   RQA_CUDA(cudaMemcpyAsync(ws->bounds, bounds, (nstripes + 1) * sizeof(int64_t),
                            cudaMemcpyHostToDevice, st),
            "copying bounds");
-  FoldArgs<int32_t> f;
-  f.P = d_prefix;
-  f.S = d_suffix;
-  f.pitch = n;
+  SymFoldArgs f;
+  memset(&f, 0, sizeof f);
+  f.sp = d_prefix;
+  f.ss = d_suffix;
+  f.scol = reinterpret_cast<const uint2*>(d_col);
   f.bounds = ws->bounds;
   f.nseg = nstripes;
+  f.rowlead = d_rowlead;
   f.n = n;
   f.hist = reinterpret_cast<unsigned long long*>(d_hist);
-  f.out_p = nullptr;
-  f.out_s = nullptr;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
-  fold_kernel<int32_t><<<(int)blocks, threads, 0, st>>>(f, kFoldFinal);
+  sym_fold_stripes<<<(int)blocks, threads, 0, st>>>(f);
   RQA_CUDA(cudaGetLastError(), "launching stitch kernel");
   g_launches++;
-  // bounds is a host array: make sure the async copy finished before return
   RQA_CUDA(cudaStreamSynchronize(st), "stitch");
   return RQA_OK;
 }
@@ -423,6 +439,8 @@ int rqa_release(void) {
     cudaSetDevice((int)d);
     cudaFree(ws->s_pad);
     cudaFree(ws->ps);
+    cudaFree(ws->cs);
+    cudaFree(ws->rowlead);
     cudaFree(ws->hist);
     cudaFree(ws->bounds);
     if (ws->init) {

@@ -58,7 +58,7 @@ struct Hist {
   unsigned long long* g;     // [3][n+1]
   int64_t stride;            // n+1
   __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
-    if (len < kSmemBins) {
+    if (sh != nullptr && len < kSmemBins) {
       atomicAdd(&sh[kind * kSmemBins + (int)len], w);
     } else {
       atomicAdd(&g[kind * stride + len], (unsigned long long)w);

@@ -7,7 +7,7 @@ namespace rqa {
 bool find_variant_m1(int m, int tau, Variant* out) {
   (void)tau;
   if (m != 1) return false;
-  *out = make_variant<kL1, 1, 1, 8, 4, 256>(0);
+  *out = make_variant<kL1, 1, 1, 8, 4>(0);
   return true;
 }
 
@@ -16,9 +16,9 @@ bool find_variant_direct(int metric, int m, int tau, Variant* out) {
   if (w > 4096) return false;  // shared-memory windows would not fit
   const int wi = (int)w;
   switch (metric) {
-    case kL1: *out = make_variant<kL1, 0, 1, 8, 4, 256>(wi); return true;
-    case kL2: *out = make_variant<kL2, 0, 1, 8, 4, 256>(wi); return true;
-    case kLinf: *out = make_variant<kLinf, 0, 1, 8, 4, 256>(wi); return true;
+    case kL1: *out = make_variant<kL1, 0, 1, 8, 4>(wi); return true;
+    case kL2: *out = make_variant<kL2, 0, 1, 8, 4>(wi); return true;
+    case kLinf: *out = make_variant<kLinf, 0, 1, 8, 4>(wi); return true;
   }
   return false;
 }

@@ -6,7 +6,7 @@ namespace rqa {
 bool find_variant_l1(int m, int tau, Variant* out) {
 #define RQA_CASE(MM, TT)                                                   \
   if (m == MM && tau == TT) {                                              \
-    *out = make_variant<kL1, MM, TT, 8, 4, 256>(0);                       \
+    *out = make_variant<kL1, MM, TT, 8, 4>(0);                       \
     return true;                                                           \
   }
   RQA_CASE(2, 1) RQA_CASE(2, 2) RQA_CASE(2, 3) RQA_CASE(3, 1) RQA_CASE(3, 2)

@@ -1,0 +1,101 @@
+// rqa_runs.cuh -- run-length monoid used to stitch vertical / white-vertical
+// lines (runs of 1s / 0s) and diagonal lines across segment boundaries.
+//
+// A segment of a sequence is summarised by its first and last maximal runs
+// (bit, length) along the traversal direction plus a "uniform" flag (the
+// whole segment is one run); runs touching neither end are counted where
+// they are found.  Combining consecutive segments is the reference's
+// carry-over rule (engine.py:287-319) made associative, and emitting the
+// end runs at the matrix border is flush_carryovers (engine.py:195-212).
+#pragma once
+#include "rqa_device.cuh"
+
+namespace rqa {
+
+// Run packed as (len << 1) | bit, len < 2^31.  len == 0: no run.
+__host__ __device__ __forceinline__ uint32_t run_pack(uint32_t len, uint32_t bit) {
+  return (len << 1) | bit;
+}
+__host__ __device__ __forceinline__ uint32_t run_len(uint32_t r) { return r >> 1; }
+__host__ __device__ __forceinline__ uint32_t run_bit(uint32_t r) { return r & 1u; }
+
+struct Seg {
+  uint32_t first, last;  // packed runs; first == 0 means empty segment
+  uint32_t uniform;      // 1: first == last and it covers the segment
+};
+
+__device__ __forceinline__ void emit_run(uint32_t r, const Hist& h) {
+  const uint32_t len = run_len(r);
+  if (len) h.add(run_bit(r) ? kVert : kWhite, len, 1u);
+}
+
+// a followed by b along the traversal direction.
+__device__ __forceinline__ Seg seg_combine(Seg a, Seg b, const Hist& h) {
+  if (a.first == 0u) return b;
+  if (b.first == 0u) return a;
+  const uint32_t al = a.last, bf = b.first;
+  Seg r;
+  if (run_bit(al) == run_bit(bf)) {
+    const uint32_t m = run_pack(run_len(al) + run_len(bf), run_bit(al));
+    if (a.uniform && b.uniform) return Seg{m, m, 1u};
+    r.first = a.uniform ? m : a.first;
+    r.last = b.uniform ? m : b.last;
+    if (!a.uniform && !b.uniform) emit_run(m, h);
+  } else {
+    r.first = a.first;
+    r.last = b.last;
+    if (!a.uniform) emit_run(al, h);
+    if (!b.uniform) emit_run(bf, h);
+  }
+  r.uniform = 0u;
+  return r;
+}
+
+// Emit every run of a segment that touches a matrix border at both ends.
+__device__ __forceinline__ void seg_flush(Seg s, const Hist& h) {
+  if (s.first == 0u) return;
+  emit_run(s.first, h);
+  if (!s.uniform) emit_run(s.last, h);
+}
+
+// Streaming state of one sequence traversed bit by bit: `first` is the first
+// run (0 while it is still open), `cur` the open run.  Interior runs are
+// emitted as soon as they close.
+struct RunState {
+  uint32_t first, cur;
+};
+
+// Consume nb (1..32) bits of x, bit 0 first.
+__device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, const Hist& h) {
+  const uint32_t full = low_mask(nb);
+  x &= full;
+  if (st.cur == 0u) st.cur = run_pack(0u, x & 1u);
+  uint32_t bit = run_bit(st.cur);
+  uint32_t diff = (bit ? ~x : x) & full;  // positions differing from the open run
+  if (diff == 0u) {
+    st.cur += (uint32_t)nb << 1;
+    return;
+  }
+  int pos = 0;
+  while (diff) {
+    const int p = __ffs(diff) - 1;  // first differing position >= pos
+    st.cur += (uint32_t)(p - pos) << 1;
+    if (st.first == 0u) st.first = st.cur;
+    else emit_run(st.cur, h);
+    bit ^= 1u;
+    st.cur = run_pack(0u, bit);
+    pos = p;
+    // next change: positions > p whose bit differs from the new run value
+    const uint32_t nd = ((bit ? ~x : x) & full);
+    diff = (p >= 31) ? 0u : (nd & (0xfffffffeu << p));
+  }
+  st.cur += (uint32_t)(nb - pos) << 1;
+}
+
+__device__ __forceinline__ Seg runs_finish(const RunState& st) {
+  if (st.cur == 0u) return Seg{0u, 0u, 0u};
+  if (st.first == 0u) return Seg{st.cur, st.cur, 1u};
+  return Seg{st.first, st.cur, 0u};
+}
+
+}  // namespace rqa

@@ -1,0 +1,452 @@
+// rqa_sym.cuh -- upper-triangle band kernel (exact symmetry R = R^T).
+//
+// Only cells with k = j - i >= 0 are evaluated: half the FP64 work of the
+// full matrix.  The lines of the full matrix are recovered exactly:
+//   * diagonal lines: diagonal -k is a copy of diagonal k (k > 0 counts 2x);
+//   * vertical / white-vertical lines: column c of the full matrix equals the
+//     "hook" c = upper column c above the diagonal (rows 0..c-1) followed by
+//     upper row c from the diagonal (columns c..n-1), because R(r,c) = R(c,r).
+// The hook's row part lives in the band holding row c (row phase); its
+// column part is cut into one segment per band (column phase) and stitched
+// by fold_hooks (rqa_fold.cuh) with the run monoid of rqa_runs.cuh.
+//
+// Geometry as in rqa_band.cuh: band of H = R*HS rows, HS = D = 32*NW,
+// iteration x covers diagonals kd = x*D - r*HS + delta in slot r, lane
+// delta = 32*warp + lane; column of step t is i0 + t + x*D + delta for every
+// slot (one shared column load feeds R cells).  Columns are met bottom-up by
+// the diagonal sweep, so the column phase consumes them bottom-up.
+#pragma once
+#include "rqa_band.cuh"
+#include "rqa_runs.cuh"
+
+namespace rqa {
+
+struct SymArgs {
+  const double* s;           // device samples (zero padded both sides)
+  int64_t len, n;
+  int64_t row_lo, row_hi;    // rows of this launch; bands start at row_lo
+  double thr;
+  int64_t theiler;
+  int m, tau;
+  uint16_t* P;               // compact [band][kd], kd in [0, n - i0): 1-run at band top
+  uint16_t* S;               // compact: 1-run at band bottom
+  uint32_t* colsum;          // compact [band][c - i0]: (top run len<<1|bit) << 16 ... see pack_col
+  uint32_t* rowlead;         // [n]: first run of upper row i from the diagonal
+  unsigned long long* hist;  // [3][n+1]
+  unsigned long long* points;
+};
+
+// Compact per-band offset of entries kd (or c - i0) in [0, n - i0).
+__host__ __device__ __forceinline__ int64_t band_offset(int64_t b, int64_t n, int64_t row_lo,
+                                                        int64_t H) {
+  return b * (n - row_lo) - H * (b * (b - 1) / 2);
+}
+
+// Column-segment summary: top and bottom runs, 15-bit lengths (H <= 32767).
+__host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot) {
+  return ((top & 0xffffu) << 16) | (bot & 0xffffu);
+}
+
+struct SymSmem {
+  int H, HS, D, W, CW;
+  size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_hist, total;
+  __host__ __device__ SymSmem(int NW, int R, int W_) {
+    D = 32 * NW;
+    HS = D;
+    H = R * HS;
+    W = W_;
+    CW = ((HS + D + W + 2) + 1) & ~1;
+    off_row = 0;
+    const size_t row_elems = ((size_t)(H + W) + 2) & ~(size_t)1;
+    off_col0 = off_row + row_elems * sizeof(double);
+    off_col1 = off_col0 + (size_t)CW * sizeof(double);
+    off_rowbuf = off_col1 + (size_t)CW * sizeof(double);
+    off_prev = off_rowbuf + (size_t)NW * H * sizeof(uint32_t);
+    off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
+    off_hist = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
+    total = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;
+  }
+};
+
+template <int METRIC, int M, int TAU, int NW, int R>
+__global__ void __launch_bounds__(NW * 32, 2)
+sym_kernel(const SymArgs a, const int W_rt) {
+  constexpr int D = 32 * NW;
+  constexpr int HS = D;
+  constexpr int H = R * HS;
+  constexpr bool kDirect = (M == 0);
+  constexpr int kW = kDirect ? 0 : (M - 1) * TAU;
+  constexpr bool kLinfAnd = (METRIC == kLinf) && (M >= 2);
+  constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
+  constexpr int NCH = HS / 32;  // == NW
+  static_assert(kW <= 32, "term window too large");
+  const int W = kDirect ? W_rt : kW;
+  const SymSmem L(NW, R, W);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* s_row = reinterpret_cast<double*>(smem + L.off_row);
+  uint32_t* rowbuf = reinterpret_cast<uint32_t*>(smem + L.off_rowbuf);
+  uint32_t* prevbuf = reinterpret_cast<uint32_t*>(smem + L.off_prev);
+  uint2* colst = reinterpret_cast<uint2*>(smem + L.off_colst);
+  uint32_t* sh_hist = reinterpret_cast<uint32_t*>(smem + L.off_hist);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_hist + 3 * kSmemBins * sizeof(uint32_t));
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wv = tid >> 5;
+  const int delta = 32 * wv + lane;
+  const int64_t n = a.n;
+  const int64_t b = blockIdx.x;
+  const int64_t i0 = a.row_lo + b * H;
+  const int64_t i_end = min(i0 + (int64_t)H, a.row_hi);
+  const int64_t nrem = n - i0;                     // diagonals present in this band
+  const int64_t X = (nrem + D - 1) / D + R - 1;
+  const double thr = a.thr;
+  const int64_t boff = band_offset(b, n, a.row_lo, H);
+  uint16_t* Pb = a.P + boff;
+  uint16_t* Sb = a.S + boff;
+  uint32_t* Cb = a.colsum + boff;
+  const Hist hist{sh_hist, a.hist, n + 1};
+  const int hrows = (int)(i_end - i0);             // valid rows of the band
+
+  for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
+  for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
+  for (int q = tid; q < 2 * H; q += NW * 32) prevbuf[q] = 0u;
+  for (int q = tid; q < NW * R * 32; q += NW * 32) colst[q] = make_uint2(0u, 0u);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double* colbuf0 = reinterpret_cast<double*>(smem + L.off_col0);
+  const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(double));
+  if (tid == 0) {
+    const double* src;
+    col_window_src(a.s, i0, &src);
+    mbar_expect_tx_arrive(&bar[0], col_bytes);
+    tma_load_1d(colbuf0, src, col_bytes, &bar[0]);
+  }
+
+  DiagRun st[R];
+  double win[R][kW > 0 ? kW : 1];
+  uint32_t ph_lo[R], ph_hi[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    st[r].len = 0;
+    st[r].rooted = 0;
+    ph_lo[r] = 0u;
+    ph_hi[r] = 0u;
+  }
+  RunState rs[R];  // row part of hook (i0 + r*HS + tid)
+#pragma unroll
+  for (int r = 0; r < R; ++r) rs[r] = RunState{0u, 0u};
+  unsigned long long pts = 0;
+
+  for (int64_t x = 0; x < X; ++x) {
+    const int64_t kx = x * D;
+    const int buf = (int)(x & 1);
+    if (tid == 0 && x + 1 < X) {
+      const double* src;
+      col_window_src(a.s, i0 + kx + D, &src);
+      double* dst = reinterpret_cast<double*>(smem + (buf ? L.off_col0 : L.off_col1));
+      mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes);
+      tma_load_1d(dst, src, col_bytes, &bar[buf ^ 1]);
+    }
+    mbar_wait(&bar[buf], (uint32_t)((x >> 1) & 1));
+    const int co = (int)((((uintptr_t)(a.s + i0 + kx)) >> 3) & 1);
+    const double* s_col =
+        reinterpret_cast<const double*>(smem + (buf ? L.off_col1 : L.off_col0)) + co + delta;
+
+    // ---- warm-up of fresh slots ------------------------------------------
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r == 0 || x == 0) {
+        const int64_t kd = kx - (int64_t)r * HS + delta;
+        st[r].len = 0;
+        st[r].rooted = (r == 0 && kd < nrem) ? 1 : 0;
+        if constexpr (!kDirect && kW > 0) {
+          if constexpr (kLinfAnd) {
+            uint32_t p = 0;
+#pragma unroll
+            for (int u = 0; u < kW; ++u)
+              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= thr) p |= 1u << u;
+            ph_lo[r] = p;
+            ph_hi[r] = 0u;
+          } else {
+#pragma unroll
+            for (int u = 0; u < kW; ++u) {
+              const double d = __dsub_rn(s_row[r * HS + u], s_col[u]);
+              win[r][u] = kSquare ? __dmul_rn(d, d) : fabs(d);
+            }
+          }
+        }
+      }
+    }
+
+    // per-slot geometry of this iteration (32-bit, relative to the slot top)
+    int kdr[R];       // kd of this lane's diagonal in slot r (may be < 0)
+    int vrows[R];     // rows of slot r inside the band (clamped to [0, HS])
+    int crows[R];     // rows of slot r whose column is < n
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t kd = kx - (int64_t)r * HS + delta;
+      kdr[r] = (int)imax64(imin64(kd, (int64_t)1 << 30), -((int64_t)1 << 30));
+      vrows[r] = (int)imax64(imin64((int64_t)hrows - (int64_t)r * HS, HS), 0);
+      crows[r] = (int)imax64(imin64(nrem - kd - (int64_t)r * HS, (int64_t)vrows[r]), 0);
+    }
+
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t dw[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) dw[r] = 0u;
+      const double* colc = s_col + 32 * c;
+      const double* rowc = s_row + 32 * c;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if constexpr (!kDirect) {
+          const double cv = colc[t + kW];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double rv = rowc[r * HS + t + kW];
+            const double d = __dsub_rn(rv, cv);
+            if constexpr (M == 1) {
+              if (fabs(d) <= thr) dw[r] |= 1u << t;
+            } else if constexpr (kLinfAnd) {
+              if (fabs(d) <= thr) {
+                if (t + kW < 32) ph_lo[r] |= 1u << ((t + kW) & 31);
+                else ph_hi[r] |= 1u << ((t + kW - 32) & 31);
+              }
+            } else {
+              const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
+              double acc = win[r][0];
+#pragma unroll
+              for (int k = 1; k < M - 1; ++k) acc = __dadd_rn(acc, win[r][k * TAU]);
+              acc = __dadd_rn(acc, term);
+              if (acc <= thr) dw[r] |= 1u << t;
+#pragma unroll
+              for (int j = 0; j + 1 < kW; ++j) win[r][j] = win[r][j + 1];
+              win[r][kW - 1] = term;
+            }
+          }
+        } else {
+          const int m = a.m, tau = a.tau;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double* rp = rowc + r * HS + t;
+            const double* cp = colc + t;
+            bool hit;
+            if (METRIC == kLinf || m == 1) {
+              hit = true;
+              for (int k = 0; k < m; ++k) hit &= (fabs(__dsub_rn(rp[k * tau], cp[k * tau])) <= thr);
+            } else {
+              double acc = 0.0;
+              for (int k = 0; k < m; ++k) {
+                const double d = __dsub_rn(rp[k * tau], cp[k * tau]);
+                const double term = (METRIC == kL2) ? __dmul_rn(d, d) : fabs(d);
+                acc = (k == 0) ? term : __dadd_rn(acc, term);
+              }
+              hit = acc <= thr;
+            }
+            if (hit) dw[r] |= 1u << t;
+          }
+        }
+      }
+
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        uint32_t word;
+        if constexpr (kLinfAnd) {
+          word = ph_lo[r];
+#pragma unroll
+          for (int k = 1; k < M; ++k) word &= __funnelshift_rc(ph_lo[r], ph_hi[r], k * TAU);
+          ph_lo[r] = ph_hi[r];
+          ph_hi[r] = 0u;
+        } else {
+          word = dw[r];
+        }
+        const int kd = kdr[r];
+        if (kd < 0 || (int64_t)kd < a.theiler) word = 0u;
+        if (kd >= 0 && (int64_t)kd < nrem) {
+          const int lb = min(max(vrows[r] - 32 * c, 0), 32);
+          const int lcb = min(max(crows[r] - 32 * c, 0), lb);
+          if ((word | (uint32_t)st[r].len | (uint32_t)st[r].rooted) != 0u || lcb < lb)
+            diag_word(word, lcb, lb, st[r], Pb + kd, kd == 0 ? 1u : 2u, hist);
+        }
+        rowbuf[wv * H + r * HS + 32 * c + lane] = transpose32(word, lane);
+      }
+    }
+    __syncthreads();
+
+    // ---- row phase: upper row i = i0 + r*HS + tid, diagonals (x-r)*D + [0, D)
+    uint32_t* prev_cur = prevbuf + buf * H;        // iteration x-1's warp NW-1 words
+    uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int lr = r * HS + tid;
+      prev_next[lr] = rowbuf[(NW - 1) * H + lr];
+      if (x >= r && lr < hrows) {
+        const int64_t gi = i0 + lr;
+        const int64_t k0 = (x - r) * (int64_t)D;          // kd of bit 0 of warp 0's word
+        const int64_t rem = (n - gi) - k0;                 // valid diagonals from k0
+        if (rem > 0) {
+          const bool first = (x == r);
+          if (rem >= D) {
+#pragma unroll
+            for (int v = 0; v < NW; ++v) {
+              const uint32_t w = rowbuf[v * H + lr];
+              pts += 2ull * __popc(w);
+              runs_consume(w, 32, rs[r], hist);
+            }
+          } else {
+            const int remi = (int)rem;
+#pragma unroll
+            for (int v = 0; v < NW; ++v) {
+              const int nb = min(max(remi - 32 * v, 0), 32);
+              if (nb > 0) {
+                const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
+                pts += 2ull * __popc(w);
+                runs_consume(w, nb, rs[r], hist);
+              }
+            }
+          }
+          if (first) pts -= (rowbuf[lr] & 1u);            // the diagonal cell counts once
+          if (rem <= D) {                                  // the row ends at column n-1
+            const Seg sg = runs_finish(rs[r]);
+            a.rowlead[gi] = sg.first;
+            if (!sg.uniform) emit_run(sg.last, hist);
+          }
+        }
+      }
+    }
+
+    // ---- column phase: warp wv owns column blocks u = wv (finishing) and
+    // u = wv + NW (starting) of every slot; lane = column.
+    {
+      Seg acc{0u, 0u, 0u};
+      const int64_t cfin = i0 + kx + 32 * wv + lane;          // finishing column
+      const int64_t cnew = cfin + D;                            // starting column
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const int r = R - 1 - rr;  // bottom-up over slots
+        uint2 cs = colst[(wv * R + r) * 32 + lane];
+        RunState cst{cs.y, cs.x};  // (first, cur)
+        if (x >= r) {
+          for (int c = wv; c >= 0; --c) {        // chunks of block u = wv, bottom-up
+            const int wp = wv - c;                // source warp of the aligned window
+            const int lr = r * HS + 32 * c + lane;
+            const uint32_t w1 = rowbuf[wp * H + lr];
+            const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lr] : prev_cur[lr];
+            const uint32_t al = __funnelshift_l(w0, w1, lane);
+            const uint32_t colw = transpose32(al, lane);
+            const int64_t row0 = i0 + (int64_t)r * HS + 32 * c;
+            const int lim = (int)imin64(imax64(imin64(cfin, i_end) - row0, 0), 32);
+            if (lim > 0 && cfin < n) {
+              const uint32_t bits = __brev(colw) >> (32 - lim);
+              runs_consume(bits, lim, cst, hist);
+            }
+          }
+        }
+        acc = seg_combine(acc, runs_finish(cst), hist);
+        // starting block u = wv + NW: chunks NW-1 .. wv+1 (lower part of the new column)
+        RunState nst{0u, 0u};
+        if (x >= r) {
+          for (int c = NCH - 1; c > wv; --c) {
+            const int wp = wv + NW - c;
+            const int lr = r * HS + 32 * c + lane;
+            const uint32_t w1 = rowbuf[wp * H + lr];
+            const uint32_t w0 = rowbuf[(wp - 1) * H + lr];
+            const uint32_t al = __funnelshift_l(w0, w1, lane);
+            const uint32_t colw = transpose32(al, lane);
+            const int64_t row0 = i0 + (int64_t)r * HS + 32 * c;
+            const int lim = (int)imin64(imax64(imin64(cnew, i_end) - row0, 0), 32);
+            if (lim > 0 && cnew < n) {
+              const uint32_t bits = __brev(colw) >> (32 - lim);
+              runs_consume(bits, lim, nst, hist);
+            }
+          }
+        }
+        colst[(wv * R + r) * 32 + lane] = make_uint2(nst.cur, nst.first);
+      }
+      // band column summary of column cfin (rows [i0, min(i_end, cfin)))
+      if (cfin < n && cfin > i0) {
+        // stored as (top run, bottom run): traversal was bottom-up
+        Cb[cfin - i0] = acc.uniform ? pack_col(acc.first, acc.first)
+                                    : pack_col(acc.last, acc.first);
+      } else if (cfin == i0) {
+        Cb[0] = 0u;
+      }
+    }
+    __syncthreads();
+
+    // ---- slot R-1 leaves the band through its bottom edge
+    {
+      const int64_t kd = kx - (int64_t)(R - 1) * HS + delta;
+      if (kd >= 0 && kd < nrem && i_end - 1 + kd < n) {
+        DiagRun& e = st[R - 1];
+        if (e.rooted) Pb[kd] = (uint16_t)e.len;
+        Sb[kd] = (uint16_t)e.len;
+      }
+    }
+    if (((x + 1) & 4095) == 0) {
+      __syncthreads();
+      for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
+        const uint32_t cnt = sh_hist[q];
+        if (cnt) {
+          atomicAdd(&a.hist[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)cnt);
+          sh_hist[q] = 0u;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = R - 1; r >= 1; --r) {
+      st[r] = st[r - 1];
+      if constexpr (!kDirect && kW > 0) {
+        if constexpr (kLinfAnd) {
+          ph_lo[r] = ph_lo[r - 1];
+        } else {
+#pragma unroll
+          for (int j = 0; j < kW; ++j) win[r][j] = win[r - 1][j];
+        }
+      }
+    }
+  }
+
+  // ---- drain diagonal slots (all remaining cells are right of column n-1)
+#pragma unroll
+  for (int dstep = 1; dstep < R; ++dstep) {
+    const int64_t kx = (X + dstep - 1) * D;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      if (r >= dstep) {
+        const int64_t kd = kx - (int64_t)r * HS + delta;
+        if (kd >= 0 && kd < nrem && i_end > i0 + (int64_t)r * HS && (st[r].len | st[r].rooted))
+          diag_end_run(st[r], Pb + kd, kd == 0 ? 1u : 2u, hist);
+      }
+    }
+    {
+      const int64_t kd = kx - (int64_t)(R - 1) * HS + delta;
+      if (kd >= 0 && kd < nrem && i_end - 1 + kd < n) {
+        DiagRun& e = st[R - 1];
+        if (e.rooted) Pb[kd] = (uint16_t)e.len;
+        Sb[kd] = (uint16_t)e.len;
+      }
+    }
+#pragma unroll
+    for (int r = R - 1; r >= 1; --r) st[r] = st[r - 1];
+    st[0].len = 0;
+    st[0].rooted = 0;
+  }
+
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) pts += __shfl_xor_sync(0xffffffffu, pts, o);
+  if (lane == 0 && pts) atomicAdd(a.points, pts);
+  __syncthreads();
+  for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
+    const uint32_t cnt = sh_hist[q];
+    if (cnt) atomicAdd(&a.hist[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)cnt);
+  }
+}
+
+}  // namespace rqa

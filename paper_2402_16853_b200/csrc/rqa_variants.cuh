@@ -1,35 +1,33 @@
 // rqa_variants.cuh -- compile-time kernel variants and their launchers.
 #pragma once
-#include "rqa_band.cuh"
+#include "rqa_sym.cuh"
 
 namespace rqa {
 
 struct Variant {
-  int nw, r, hs;          // warps per CTA, stacked slots, slot height
+  int nw, r;              // warps per CTA, stacked slots (band = r * 32 * nw rows)
   int w;                  // term window (m-1)*tau
   int reuse;              // 1: compile-time (m, tau) with term reuse; 0: direct
   size_t smem;            // dynamic shared memory bytes
-  cudaError_t (*launch)(const BandArgs&, int nbands, int w, cudaStream_t);
-  int64_t band_rows() const { return (int64_t)r * hs; }
+  cudaError_t (*launch)(const SymArgs&, int nbands, int w, cudaStream_t);
+  int64_t band_rows() const { return (int64_t)r * 32 * nw; }
 };
 
-template <int METRIC, int M, int TAU, int NW, int R, int HS>
-cudaError_t launch_band(const BandArgs& a, int nbands, int w, cudaStream_t st) {
-  using C = BandCfg<METRIC, M, TAU, NW, R, HS>;
-  const BandSmem L(NW, R, HS, C::kDirect ? w : C::kW);
-  auto k = band_kernel<METRIC, M, TAU, NW, R, HS>;
+template <int METRIC, int M, int TAU, int NW, int R>
+cudaError_t launch_sym(const SymArgs& a, int nbands, int w, cudaStream_t st) {
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
+  auto k = sym_kernel<METRIC, M, TAU, NW, R>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   k<<<nbands, NW * 32, L.total, st>>>(a, w);
   return cudaGetLastError();
 }
 
-template <int METRIC, int M, int TAU, int NW, int R, int HS>
+template <int METRIC, int M, int TAU, int NW, int R>
 Variant make_variant(int w_rt) {
-  using C = BandCfg<METRIC, M, TAU, NW, R, HS>;
-  const int w = C::kDirect ? w_rt : C::kW;
-  const BandSmem L(NW, R, HS, w);
-  return Variant{NW, R, HS, w, C::kDirect ? 0 : 1, L.total, &launch_band<METRIC, M, TAU, NW, R, HS>};
+  const int w = (M == 0) ? w_rt : (M - 1) * TAU;
+  const SymSmem L(NW, R, w);
+  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_sym<METRIC, M, TAU, NW, R>};
 }
 
 // Implemented in rqa_kernels_<metric>.cu (one translation unit per metric so

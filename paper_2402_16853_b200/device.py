@@ -5,11 +5,13 @@ done by librqa_b200.so through the C-ABI (rqa_run_device / rqa_stitch_device).
 """
 
 import ctypes
+from dataclasses import dataclass
 
 from . import _native
 from .settings import METRIC_CODES, AnalysisSettings
 
-__all__ = ["band_rows", "run_rows_device", "stitch_device", "MODE_FINAL", "MODE_STRIPE"]
+__all__ = ["band_rows", "run_rows_device", "stitch_device", "StripeOutputs", "MODE_FINAL",
+           "MODE_STRIPE"]
 
 MODE_FINAL = 0
 MODE_STRIPE = 1
@@ -26,12 +28,33 @@ def band_rows(settings: AnalysisSettings) -> int:
     return int(h.value)
 
 
+@dataclass
+class StripeOutputs:
+    """Per-stripe summaries of a multi-GPU run (see include/rqa_b200.h)."""
+
+    prefix: object   # int32 [n]
+    suffix: object   # int32 [n]
+    col: object      # int32 [2n] (uint32 bit patterns)
+    rowlead: object  # int32 [n] (uint32 bit patterns), zero-initialised
+
+    @staticmethod
+    def empty(n: int, device, rows: int = 1):
+        import torch
+
+        shape = (rows, n) if rows > 1 else (n,)
+        cshape = (rows, 2 * n) if rows > 1 else (2 * n,)
+        return StripeOutputs(torch.zeros(shape, dtype=torch.int32, device=device),
+                             torch.zeros(shape, dtype=torch.int32, device=device),
+                             torch.zeros(cshape, dtype=torch.int32, device=device),
+                             torch.zeros(n, dtype=torch.int32, device=device))
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
 def run_rows_device(series, settings: AnalysisSettings, row_lo: int, row_hi: int, mode: int,
-                    hist, points, stripe_prefix=None, stripe_suffix=None, stream=None) -> None:
+                    hist, points, stripe: StripeOutputs | None = None, stream=None) -> None:
     """Enqueue the band + fold kernels for rows [row_lo, row_hi) on ``stream``.
 
     series: float64 CUDA tensor of samples; hist: int64 CUDA tensor [3, n+1]
@@ -41,20 +64,22 @@ def run_rows_device(series, settings: AnalysisSettings, row_lo: int, row_hi: int
 
     if stream is None:
         stream = torch.cuda.current_stream(series.device)
+    so = stripe if stripe is not None else StripeOutputs(None, None, None, None)
     _native.call("rqa_run_device", _ptr(series), series.numel(),
                  settings.embedding_dimension, settings.time_delay,
                  METRIC_CODES[settings.metric], float(settings.radius),
                  settings.theiler_window, int(row_lo), int(row_hi), int(mode),
-                 _ptr(hist), _ptr(points), _ptr(stripe_prefix), _ptr(stripe_suffix),
-                 ctypes.c_void_p(stream.cuda_stream))
+                 _ptr(hist), _ptr(points), _ptr(so.prefix), _ptr(so.suffix), _ptr(so.col),
+                 _ptr(so.rowlead), ctypes.c_void_p(stream.cuda_stream))
 
 
-def stitch_device(prefix, suffix, bounds, n: int, hist, stream=None) -> None:
-    """Fold the gathered stripe summaries ([G, n] int32 CUDA) into hist."""
+def stitch_device(gathered: StripeOutputs, bounds, n: int, hist, stream=None) -> None:
+    """Fold the gathered stripe summaries ([G, n] / [G, 2n] / summed rowlead) into hist."""
     import torch
 
     if stream is None:
-        stream = torch.cuda.current_stream(prefix.device)
+        stream = torch.cuda.current_stream(gathered.prefix.device)
     b = (ctypes.c_int64 * len(bounds))(*[int(x) for x in bounds])
-    _native.call("rqa_stitch_device", _ptr(prefix), _ptr(suffix), b, len(bounds) - 1, int(n),
+    _native.call("rqa_stitch_device", _ptr(gathered.prefix), _ptr(gathered.suffix),
+                 _ptr(gathered.col), _ptr(gathered.rowlead), b, len(bounds) - 1, int(n),
                  _ptr(hist), ctypes.c_void_p(stream.cuda_stream))

@@ -24,32 +24,60 @@ __all__ = ["stripe_bounds", "run_analysis_distributed", "gpu_stripe_fn", "gpu_st
 
 
 def stripe_bounds(n: int, world: int, band: int) -> list:
-    """Equal-work row stripes aligned to ``band`` rows: world+1 boundaries."""
-    nb = -(-n // band)
-    out = []
-    for r in range(world + 1):
-        out.append(min(n, (nb * r // world) * band))
-    out[-1] = n
+    """Equal-work row stripes aligned to ``band`` rows: world+1 boundaries.
+
+    Only the upper triangle is evaluated, so row i costs n - i cells; the
+    boundaries split the triangle's area evenly (i_g = n (1 - sqrt(1 - g/G))),
+    rounded to band multiples, monotone.
+    """
+    import math
+
+    out = [0]
+    for g in range(1, world):
+        i = n * (1.0 - math.sqrt(1.0 - g / world))
+        b = int(round(i / band)) * band
+        out.append(max(out[-1], min(n, b)))
+    out.append(n)
     return out
 
 
 def gpu_stripe_fn(series_dev, settings, lo, hi, n, device):
+    """This rank's stripe on its GPU: (hist [3,n+1], points [1], StripeOutputs)."""
     import torch
 
-    from .device import MODE_STRIPE, run_rows_device
+    from .device import MODE_STRIPE, StripeOutputs, run_rows_device
 
     hist = torch.zeros(3, n + 1, dtype=torch.int64, device=device)
     points = torch.zeros(1, dtype=torch.int64, device=device)
-    pre = torch.zeros(n, dtype=torch.int32, device=device)
-    suf = torch.zeros(n, dtype=torch.int32, device=device)
-    run_rows_device(series_dev, settings, lo, hi, MODE_STRIPE, hist, points, pre, suf)
-    return hist, points, pre, suf
+    so = StripeOutputs.empty(n, device)
+    run_rows_device(series_dev, settings, lo, hi, MODE_STRIPE, hist, points, so)
+    return hist, points, so
 
 
-def gpu_stitch_fn(pre_all, suf_all, bounds, n, hist):
+def gpu_stitch_fn(gathered, bounds, n, hist):
     from .device import stitch_device
 
-    stitch_device(pre_all, suf_all, bounds, n, hist)
+    stitch_device(gathered, bounds, n, hist)
+
+
+def exchange(so, world, group=None):
+    """All-gather the stripe edge summaries, sum the row leads (disjoint rows)."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import StripeOutputs
+
+    n = so.prefix.numel()
+    dev = so.prefix.device
+    out = StripeOutputs(torch.empty(world, n, dtype=so.prefix.dtype, device=dev),
+                        torch.empty(world, n, dtype=so.suffix.dtype, device=dev),
+                        torch.empty(world, 2 * n, dtype=so.col.dtype, device=dev),
+                        so.rowlead)
+    dist.all_gather_into_tensor(out.prefix, so.prefix, group=group)
+    dist.all_gather_into_tensor(out.suffix, so.suffix, group=group)
+    dist.all_gather_into_tensor(out.col, so.col, group=group)
+    dist.all_reduce(out.rowlead, group=group)
+    return out
 
 
 def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSettings, *,
@@ -78,15 +106,12 @@ def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSetting
         band = band_rows(settings)
     bounds = stripe_bounds(n, world, band)
     series = torch.from_numpy(np.ascontiguousarray(embedded.values, np.float64)).to(device)
-    hist, points, pre, suf = stripe_fn(series, settings, bounds[rank], bounds[rank + 1], n, device)
-    pre_all = torch.empty(world, n, dtype=pre.dtype, device=device)
-    suf_all = torch.empty(world, n, dtype=suf.dtype, device=device)
-    dist.all_gather_into_tensor(pre_all, pre, group=group)
-    dist.all_gather_into_tensor(suf_all, suf, group=group)
+    hist, points, so = stripe_fn(series, settings, bounds[rank], bounds[rank + 1], n, device)
+    gathered = exchange(so, world, group)
     dist.reduce(hist, dst=0, group=group)
     dist.reduce(points, dst=0, group=group)
     if rank != 0:
         return None
-    stitch_fn(pre_all, suf_all, bounds, n, hist)
+    stitch_fn(gathered, bounds, n, hist)
     h = hist.cpu().numpy()
     return LineHistograms(n, int(points.cpu().item()), h[0].copy(), h[1].copy(), h[2].copy())

@@ -162,13 +162,13 @@ def test_stripes_then_stitch_equal_single_run():
     """Multi-GPU decomposition, emulated on one device: G stripes + stitch."""
     import torch
 
-    from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, band_rows,
+    from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, StripeOutputs, band_rows,
                                               run_rows_device, stitch_device)
     from paper_2402_16853_b200.distributed import stripe_bounds
 
     rng = np.random.default_rng(11)
     for metric, m, tau, r, length in (("l2", 3, 1, 0.12, 9000), ("linf", 2, 2, 0.3, 7001),
-                                      ("l1", 1, 1, 0.02, 5000)):
+                                      ("l1", 1, 1, 0.02, 5000), ("l1", 6, 2, 0.5, 4100)):
         s = np.sin(np.linspace(0, 30 * np.pi, length)) + 0.2 * rng.uniform(-1, 1, length)
         st = AnalysisSettings(m, tau, metric, r)
         n = length - (m - 1) * tau
@@ -182,11 +182,12 @@ def test_stripes_then_stitch_equal_single_run():
             bounds = stripe_bounds(n, g, band)
             h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
             p = torch.zeros(1, dtype=torch.int64, device=dev)
-            pre = torch.zeros(g, n, dtype=torch.int32, device=dev)
-            suf = torch.zeros(g, n, dtype=torch.int32, device=dev)
+            gathered = StripeOutputs.empty(n, dev, rows=g)
             for q in range(g):
-                run_rows_device(sd, st, bounds[q], bounds[q + 1], MODE_STRIPE, h, p, pre[q], suf[q])
-            stitch_device(pre, suf, bounds, n, h)
+                so = StripeOutputs(gathered.prefix[q], gathered.suffix[q], gathered.col[q],
+                                   gathered.rowlead)
+                run_rows_device(sd, st, bounds[q], bounds[q + 1], MODE_STRIPE, h, p, so)
+            stitch_device(gathered, bounds, n, h)
             torch.cuda.synchronize()
             assert torch.equal(h, ref_h), (metric, g)
             assert torch.equal(p, ref_p)
