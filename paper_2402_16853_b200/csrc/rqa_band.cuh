@@ -132,7 +132,7 @@ band_kernel(const BandArgs a, const int W_rt) {
   const double thr = a.thr;
   uint16_t* Pb = a.P + (int64_t)blockIdx.x * n;
   uint16_t* Sb = a.S + (int64_t)blockIdx.x * n;
-  const Hist hist{sh_hist, a.hist, n + 1};
+  const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
 
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
   for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];

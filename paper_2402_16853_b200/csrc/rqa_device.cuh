@@ -46,6 +46,41 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
+// Per-lane constants of the rotate-and-select 32x32 bit transpose: stage j
+// exchanges j-blocks with lane^j; the partner word is rotated left by j (or
+// 32-j when lane bit j is set) and bit-selected into place with mask M_j.
+struct Transposer {
+  uint32_t M[5];
+  uint32_t amt[5];
+  __device__ __forceinline__ explicit Transposer(int lane) {
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int j = 16 >> s;
+      const uint32_t m = (j == 16) ? 0x0000FFFFu
+                       : (j == 8)  ? 0x00FF00FFu
+                       : (j == 4)  ? 0x0F0F0F0Fu
+                       : (j == 2)  ? 0x33333333u
+                                   : 0x55555555u;
+      const bool hi = (lane & j) != 0;
+      M[s] = hi ? m : ~m;
+      amt[s] = hi ? (uint32_t)(32 - j) : (uint32_t)j;
+    }
+  }
+  // lane l word bit t -> lane t word bit l
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int j = 16 >> s;
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const uint32_t r = (j == 16) ? __funnelshift_l(y, y, 16) : __funnelshift_l(y, y, amt[s]);
+      uint32_t o;  // bit select (x & ~M) | (r & M) in one LOP3
+      asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(o) : "r"(x), "r"(r), "r"(M[s]));
+      x = o;
+    }
+    return x;
+  }
+};
+
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
@@ -53,16 +88,29 @@ __device__ __forceinline__ uint32_t low_mask(int bits) {
   return bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
 }
 
+// Line-length histograms of one CTA: 32-bit shared-memory bins for lengths
+// < kSmemBins (red.shared, no generic addressing), 64-bit global atomics
+// beyond.  kind: kDiag, kVert, kWhite.
 struct Hist {
-  uint32_t* sh;              // [3][kSmemBins]
+  uint32_t sh;               // shared-window address of [3][kSmemBins] u32 bins
   unsigned long long* g;     // [3][n+1]
   int64_t stride;            // n+1
   __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
-    if (sh != nullptr && len < kSmemBins) {
-      atomicAdd(&sh[kind * kSmemBins + (int)len], w);
+    if (len < kSmemBins) {
+      const uint32_t addr = sh + 4u * (uint32_t)(kind * kSmemBins + (int)len);
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
     } else {
       atomicAdd(&g[kind * stride + len], (unsigned long long)w);
     }
+  }
+};
+
+// Global-only histogram (fold kernels).
+struct GHist {
+  unsigned long long* g;
+  int64_t stride;
+  __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
+    atomicAdd(&g[kind * stride + len], (unsigned long long)w);
   }
 };
 

@@ -154,7 +154,7 @@ __global__ void sym_fold_diag(const SymFoldArgs a, const int mode) {
   }
 }
 
-__device__ __forceinline__ void hook_finish(Seg acc, uint32_t lead, const Hist& h) {
+__device__ __forceinline__ void hook_finish(Seg acc, uint32_t lead, const GHist& h) {
   if (acc.first == 0u) {
     emit_run(lead, h);
     return;
@@ -174,7 +174,7 @@ __device__ __forceinline__ void hook_finish(Seg acc, uint32_t lead, const Hist& 
 // of [row_lo, row_hi) above row c, then (final mode) the row part's lead.
 __global__ void sym_fold_hooks(const SymFoldArgs a, const int mode) {
   const int64_t n = a.n;
-  const Hist h{nullptr, a.hist, n + 1};
+  const GHist h{a.hist, n + 1};
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
     Seg acc{0u, 0u, 0u};
@@ -199,7 +199,7 @@ __global__ void sym_fold_hooks(const SymFoldArgs a, const int mode) {
 // Final fold over stripes (multi-GPU): diagonals and hooks.
 __global__ void sym_fold_stripes(const SymFoldArgs a) {
   const int64_t n = a.n;
-  const Hist h{nullptr, a.hist, n + 1};
+  const GHist h{a.hist, n + 1};
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     // diagonal k

@@ -24,13 +24,15 @@ struct Seg {
   uint32_t uniform;      // 1: first == last and it covers the segment
 };
 
-__device__ __forceinline__ void emit_run(uint32_t r, const Hist& h) {
+template <class HistT>
+__device__ __forceinline__ void emit_run(uint32_t r, const HistT& h) {
   const uint32_t len = run_len(r);
   if (len) h.add(run_bit(r) ? kVert : kWhite, len, 1u);
 }
 
 // a followed by b along the traversal direction.
-__device__ __forceinline__ Seg seg_combine(Seg a, Seg b, const Hist& h) {
+template <class HistT>
+__device__ __forceinline__ Seg seg_combine(Seg a, Seg b, const HistT& h) {
   if (a.first == 0u) return b;
   if (b.first == 0u) return a;
   const uint32_t al = a.last, bf = b.first;
@@ -52,7 +54,8 @@ __device__ __forceinline__ Seg seg_combine(Seg a, Seg b, const Hist& h) {
 }
 
 // Emit every run of a segment that touches a matrix border at both ends.
-__device__ __forceinline__ void seg_flush(Seg s, const Hist& h) {
+template <class HistT>
+__device__ __forceinline__ void seg_flush(Seg s, const HistT& h) {
   if (s.first == 0u) return;
   emit_run(s.first, h);
   if (!s.uniform) emit_run(s.last, h);
@@ -65,31 +68,44 @@ struct RunState {
   uint32_t first, cur;
 };
 
-// Consume nb (1..32) bits of x, bit 0 first.
-__device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, const Hist& h) {
+// Where closed runs go: vertical/white-vertical lines (both bit values) or
+// diagonal lines (only runs of ones, with weight 2 for k > 0 by symmetry).
+struct LineSink {
+  const Hist* h;
+  uint32_t diag_weight;  // 0: row/column sink; 1 or 2: diagonal sink
+  __device__ __forceinline__ void operator()(uint32_t run) const {
+    const uint32_t len = run_len(run);
+    if (diag_weight == 0u) {
+      h->add(run_bit(run) ? kVert : kWhite, len, 1u);
+    } else if (run_bit(run)) {
+      h->add(kDiag, len, diag_weight);
+    }
+  }
+};
+
+// Consume nb (1..32) bits of x, bit 0 first.  Run boundaries are the set
+// bits of x ^ (x << 1 | carried bit); each one closes the open run.
+__device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, const LineSink& sink) {
   const uint32_t full = low_mask(nb);
   x &= full;
-  if (st.cur == 0u) st.cur = run_pack(0u, x & 1u);
-  uint32_t bit = run_bit(st.cur);
-  uint32_t diff = (bit ? ~x : x) & full;  // positions differing from the open run
-  if (diff == 0u) {
-    st.cur += (uint32_t)nb << 1;
+  uint32_t cur = st.cur;
+  if (cur == 0u) cur = x & 1u;                         // sequence starts here
+  uint32_t bnd = (x ^ ((x << 1) | (cur & 1u))) & full;
+  if (bnd == 0u) {                                     // fast path: no boundary
+    st.cur = cur + ((uint32_t)nb << 1);
     return;
   }
-  int pos = 0;
-  while (diff) {
-    const int p = __ffs(diff) - 1;  // first differing position >= pos
-    st.cur += (uint32_t)(p - pos) << 1;
-    if (st.first == 0u) st.first = st.cur;
-    else emit_run(st.cur, h);
-    bit ^= 1u;
-    st.cur = run_pack(0u, bit);
+  uint32_t pos = 0;
+  do {
+    const uint32_t p = (uint32_t)__ffs(bnd) - 1u;
+    const uint32_t run = cur + ((p - pos) << 1);
+    if (st.first == 0u) st.first = run;
+    else sink(run);
+    cur = (cur & 1u) ^ 1u;
     pos = p;
-    // next change: positions > p whose bit differs from the new run value
-    const uint32_t nd = ((bit ? ~x : x) & full);
-    diff = (p >= 31) ? 0u : (nd & (0xfffffffeu << p));
-  }
-  st.cur += (uint32_t)(nb - pos) << 1;
+    bnd &= bnd - 1u;
+  } while (bnd);
+  st.cur = cur + (((uint32_t)nb - pos) << 1);
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {

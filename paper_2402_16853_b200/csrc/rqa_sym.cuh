@@ -68,6 +68,29 @@ struct SymSmem {
   }
 };
 
+// Set bit T of dw iff acc <= thr: DSETP + predicated LOP3 (no SEL chains).
+__device__ __forceinline__ void setbit_le(uint32_t& dw, double acc, double thr, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+      : "+r"(dw)
+      : "d"(acc), "d"(thr), "r"(bit));
+}
+
+// A diagonal's segment inside the band ends: report its band-top run as P
+// (length if it is a run of ones, else 0) and, if the segment ends at the
+// band's bottom edge (open), its bottom run as S; a segment cut by the
+// matrix's right edge (closed) counts its last run here.
+__device__ __forceinline__ void diag_finish(const RunState& st, bool open, uint16_t* Pk,
+                                            uint16_t* Sk, const LineSink& sink) {
+  const Seg g = runs_finish(st);
+  const uint32_t first = g.first;
+  *Pk = (uint16_t)(run_bit(first) ? run_len(first) : 0u);
+  if (open) {
+    *Sk = (uint16_t)(run_bit(g.last) ? run_len(g.last) : 0u);
+  } else if (!g.uniform) {
+    sink(g.last);
+  }
+}
+
 template <int METRIC, int M, int TAU, int NW, int R>
 __global__ void __launch_bounds__(NW * 32, 2)
 sym_kernel(const SymArgs a, const int W_rt) {
@@ -99,15 +122,19 @@ sym_kernel(const SymArgs a, const int W_rt) {
   const int64_t b = blockIdx.x;
   const int64_t i0 = a.row_lo + b * H;
   const int64_t i_end = min(i0 + (int64_t)H, a.row_hi);
-  const int64_t nrem = n - i0;                     // diagonals present in this band
-  const int64_t X = (nrem + D - 1) / D + R - 1;
+  const int nrem = (int)(n - i0);                  // diagonals (and columns) present in the band
+  const int X = (nrem + D - 1) / D + R - 1;
+  const int hrows = (int)(i_end - i0);             // valid rows of the band
+  const int bot_rows = (int)(n - i_end) + 1;       // kd < bot_rows <=> bottom row valid
+  const int theiler = (int)min(a.theiler, (int64_t)1 << 30);
   const double thr = a.thr;
   const int64_t boff = band_offset(b, n, a.row_lo, H);
   uint16_t* Pb = a.P + boff;
   uint16_t* Sb = a.S + boff;
   uint32_t* Cb = a.colsum + boff;
-  const Hist hist{sh_hist, a.hist, n + 1};
-  const int hrows = (int)(i_end - i0);             // valid rows of the band
+  uint32_t* lead_out = a.rowlead + i0;
+  const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
+  const Transposer tr(lane);
 
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
   for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
@@ -119,39 +146,38 @@ sym_kernel(const SymArgs a, const int W_rt) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  double* colbuf0 = reinterpret_cast<double*>(smem + L.off_col0);
   const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(double));
   if (tid == 0) {
     const double* src;
     col_window_src(a.s, i0, &src);
     mbar_expect_tx_arrive(&bar[0], col_bytes);
-    tma_load_1d(colbuf0, src, col_bytes, &bar[0]);
+    tma_load_1d(smem + L.off_col0, src, col_bytes, &bar[0]);
   }
 
-  DiagRun st[R];
+  RunState st[R];  // diagonal run state per slot (first run = band-top run)
   double win[R][kW > 0 ? kW : 1];
   uint32_t ph_lo[R], ph_hi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    st[r].len = 0;
-    st[r].rooted = 0;
+    st[r] = RunState{0u, 0u};
     ph_lo[r] = 0u;
     ph_hi[r] = 0u;
   }
+  const LineSink vsink{&hist, 0u};
   RunState rs[R];  // row part of hook (i0 + r*HS + tid)
 #pragma unroll
   for (int r = 0; r < R; ++r) rs[r] = RunState{0u, 0u};
-  unsigned long long pts = 0;
+  uint32_t pts = 0;  // per-thread partial, flushed to 64 bits every iteration
 
-  for (int64_t x = 0; x < X; ++x) {
-    const int64_t kx = x * D;
-    const int buf = (int)(x & 1);
+  unsigned long long pts64 = 0;
+  for (int x = 0; x < X; ++x) {
+    const int kx = x * D;
+    const int buf = x & 1;
     if (tid == 0 && x + 1 < X) {
       const double* src;
       col_window_src(a.s, i0 + kx + D, &src);
-      double* dst = reinterpret_cast<double*>(smem + (buf ? L.off_col0 : L.off_col1));
       mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes);
-      tma_load_1d(dst, src, col_bytes, &bar[buf ^ 1]);
+      tma_load_1d(smem + (buf ? L.off_col0 : L.off_col1), src, col_bytes, &bar[buf ^ 1]);
     }
     mbar_wait(&bar[buf], (uint32_t)((x >> 1) & 1));
     const int co = (int)((((uintptr_t)(a.s + i0 + kx)) >> 3) & 1);
@@ -162,9 +188,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r == 0 || x == 0) {
-        const int64_t kd = kx - (int64_t)r * HS + delta;
-        st[r].len = 0;
-        st[r].rooted = (r == 0 && kd < nrem) ? 1 : 0;
+        st[r] = RunState{0u, 0u};
         if constexpr (!kDirect && kW > 0) {
           if constexpr (kLinfAnd) {
             uint32_t p = 0;
@@ -184,16 +208,18 @@ sym_kernel(const SymArgs a, const int W_rt) {
       }
     }
 
-    // per-slot geometry of this iteration (32-bit, relative to the slot top)
-    int kdr[R];       // kd of this lane's diagonal in slot r (may be < 0)
-    int vrows[R];     // rows of slot r inside the band (clamped to [0, HS])
-    int crows[R];     // rows of slot r whose column is < n
+    // per-slot geometry of this iteration, relative to the slot's first row
+    int kdr[R];     // kd of this lane's diagonal in slot r (may be < 0)
+    int lastc[R];   // rows [0, lastc) of slot r are valid cells of the diagonal
+    int openb[R];   // 1: the diagonal continues past the slot's valid rows into the next band
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int64_t kd = kx - (int64_t)r * HS + delta;
-      kdr[r] = (int)imax64(imin64(kd, (int64_t)1 << 30), -((int64_t)1 << 30));
-      vrows[r] = (int)imax64(imin64((int64_t)hrows - (int64_t)r * HS, HS), 0);
-      crows[r] = (int)imax64(imin64(nrem - kd - (int64_t)r * HS, (int64_t)vrows[r]), 0);
+      const int kd = kx - r * HS + delta;
+      kdr[r] = kd;
+      const int vrows = min(max(hrows - r * HS, 0), HS);
+      const int crows = min(max(nrem - kd - r * HS, 0), vrows);
+      lastc[r] = crows;
+      openb[r] = (crows == vrows) ? 1 : 0;
     }
 
     for (int c = 0; c < NCH; ++c) {
@@ -211,7 +237,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
             const double rv = rowc[r * HS + t + kW];
             const double d = __dsub_rn(rv, cv);
             if constexpr (M == 1) {
-              if (fabs(d) <= thr) dw[r] |= 1u << t;
+              setbit_le(dw[r], fabs(d), thr, 1u << t);
             } else if constexpr (kLinfAnd) {
               if (fabs(d) <= thr) {
                 if (t + kW < 32) ph_lo[r] |= 1u << ((t + kW) & 31);
@@ -223,7 +249,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
 #pragma unroll
               for (int k = 1; k < M - 1; ++k) acc = __dadd_rn(acc, win[r][k * TAU]);
               acc = __dadd_rn(acc, term);
-              if (acc <= thr) dw[r] |= 1u << t;
+              setbit_le(dw[r], acc, thr, 1u << t);
 #pragma unroll
               for (int j = 0; j + 1 < kW; ++j) win[r][j] = win[r][j + 1];
               win[r][kW - 1] = term;
@@ -266,130 +292,107 @@ sym_kernel(const SymArgs a, const int W_rt) {
           word = dw[r];
         }
         const int kd = kdr[r];
-        if (kd < 0 || (int64_t)kd < a.theiler) word = 0u;
-        if (kd >= 0 && (int64_t)kd < nrem) {
-          const int lb = min(max(vrows[r] - 32 * c, 0), 32);
-          const int lcb = min(max(crows[r] - 32 * c, 0), lb);
-          if ((word | (uint32_t)st[r].len | (uint32_t)st[r].rooted) != 0u || lcb < lb)
-            diag_word(word, lcb, lb, st[r], Pb + kd, kd == 0 ? 1u : 2u, hist);
+        if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
+        // diagonal runs: bits [0, lc) are cells; the segment is cut by the
+        // matrix's right edge in the chunk holding relative row lastc (unless
+        // it runs down to the band's last row: openb)
+        if (kd >= 0 && kd < nrem) {
+          const int rel = lastc[r] - 32 * c;
+          if (rel > 0) runs_consume(word, min(rel, 32), st[r], LineSink{&hist, kd == 0 ? 1u : 2u});
+          if (!openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+            diag_finish(st[r], false, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
+            st[r] = RunState{1u, 0u};  // finished: later slots of this diagonal are empty
+          }
         }
-        rowbuf[wv * H + r * HS + 32 * c + lane] = transpose32(word, lane);
+        rowbuf[wv * H + r * HS + 32 * c + lane] = tr(word);
       }
     }
     __syncthreads();
 
     // ---- row phase: upper row i = i0 + r*HS + tid, diagonals (x-r)*D + [0, D)
-    uint32_t* prev_cur = prevbuf + buf * H;        // iteration x-1's warp NW-1 words
+    const uint32_t* prev_cur = prevbuf + buf * H;   // iteration x-1's warp NW-1 words
     uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int lr = r * HS + tid;
       prev_next[lr] = rowbuf[(NW - 1) * H + lr];
       if (x >= r && lr < hrows) {
-        const int64_t gi = i0 + lr;
-        const int64_t k0 = (x - r) * (int64_t)D;          // kd of bit 0 of warp 0's word
-        const int64_t rem = (n - gi) - k0;                 // valid diagonals from k0
+        const int rem = nrem - lr - (x - r) * D;      // valid diagonals of this row from k0
         if (rem > 0) {
-          const bool first = (x == r);
-          if (rem >= D) {
-#pragma unroll
+          if (rem > D) {
+#pragma unroll 4
             for (int v = 0; v < NW; ++v) {
               const uint32_t w = rowbuf[v * H + lr];
-              pts += 2ull * __popc(w);
-              runs_consume(w, 32, rs[r], hist);
+              pts += __popc(w);
+              runs_consume(w, 32, rs[r], vsink);
             }
           } else {
-            const int remi = (int)rem;
-#pragma unroll
-            for (int v = 0; v < NW; ++v) {
-              const int nb = min(max(remi - 32 * v, 0), 32);
-              if (nb > 0) {
-                const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
-                pts += 2ull * __popc(w);
-                runs_consume(w, nb, rs[r], hist);
-              }
+            for (int v = 0; 32 * v < rem; ++v) {
+              const int nb = min(rem - 32 * v, 32);
+              const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
+              pts += __popc(w);
+              runs_consume(w, nb, rs[r], vsink);
             }
-          }
-          if (first) pts -= (rowbuf[lr] & 1u);            // the diagonal cell counts once
-          if (rem <= D) {                                  // the row ends at column n-1
-            const Seg sg = runs_finish(rs[r]);
-            a.rowlead[gi] = sg.first;
+            const Seg sg = runs_finish(rs[r]);      // the row ends at column n-1
+            lead_out[lr] = sg.first;
             if (!sg.uniform) emit_run(sg.last, hist);
           }
+          if (x == r) pts64 -= (rowbuf[lr] & 1u);      // the diagonal cell counts once
         }
       }
     }
+    pts64 += 2ull * pts;
+    pts = 0;
 
-    // ---- column phase: warp wv owns column blocks u = wv (finishing) and
-    // u = wv + NW (starting) of every slot; lane = column.
+    // ---- column phase: warp wv finishes column block u = wv (chunks wv..0)
+    // and starts block u = wv + NW (chunks NW-1..wv+1) of every slot; lane =
+    // column; rows are consumed bottom-up.
     {
       Seg acc{0u, 0u, 0u};
-      const int64_t cfin = i0 + kx + 32 * wv + lane;          // finishing column
-      const int64_t cnew = cfin + D;                            // starting column
+      const int cfin = kx + 32 * wv + lane;      // finishing column, relative to i0
+      const int cnew = cfin + D;                  // starting column
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        const int r = R - 1 - rr;  // bottom-up over slots
+        const int r = R - 1 - rr;
         uint2 cs = colst[(wv * R + r) * 32 + lane];
-        RunState cst{cs.y, cs.x};  // (first, cur)
+        RunState fin{cs.y, cs.x};
+        RunState nst{0u, 0u};
         if (x >= r) {
-          for (int c = wv; c >= 0; --c) {        // chunks of block u = wv, bottom-up
-            const int wp = wv - c;                // source warp of the aligned window
+          for (int c = NCH - 1; c >= 0; --c) {
+            const bool finishing = c <= wv;
+            const int wp = finishing ? wv - c : wv + NW - c;
             const int lr = r * HS + 32 * c + lane;
             const uint32_t w1 = rowbuf[wp * H + lr];
             const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lr] : prev_cur[lr];
-            const uint32_t al = __funnelshift_l(w0, w1, lane);
-            const uint32_t colw = transpose32(al, lane);
-            const int64_t row0 = i0 + (int64_t)r * HS + 32 * c;
-            const int lim = (int)imin64(imax64(imin64(cfin, i_end) - row0, 0), 32);
-            if (lim > 0 && cfin < n) {
+            const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
+            const int col = finishing ? cfin : cnew;
+            const int lim = min(max(min(col, hrows) - (r * HS + 32 * c), 0), 32);
+            if (lim > 0 && col < nrem) {
               const uint32_t bits = __brev(colw) >> (32 - lim);
-              runs_consume(bits, lim, cst, hist);
+              if (finishing) runs_consume(bits, lim, fin, vsink);
+              else runs_consume(bits, lim, nst, vsink);
             }
           }
         }
-        acc = seg_combine(acc, runs_finish(cst), hist);
-        // starting block u = wv + NW: chunks NW-1 .. wv+1 (lower part of the new column)
-        RunState nst{0u, 0u};
-        if (x >= r) {
-          for (int c = NCH - 1; c > wv; --c) {
-            const int wp = wv + NW - c;
-            const int lr = r * HS + 32 * c + lane;
-            const uint32_t w1 = rowbuf[wp * H + lr];
-            const uint32_t w0 = rowbuf[(wp - 1) * H + lr];
-            const uint32_t al = __funnelshift_l(w0, w1, lane);
-            const uint32_t colw = transpose32(al, lane);
-            const int64_t row0 = i0 + (int64_t)r * HS + 32 * c;
-            const int lim = (int)imin64(imax64(imin64(cnew, i_end) - row0, 0), 32);
-            if (lim > 0 && cnew < n) {
-              const uint32_t bits = __brev(colw) >> (32 - lim);
-              runs_consume(bits, lim, nst, hist);
-            }
-          }
-        }
+        acc = seg_combine(acc, runs_finish(fin), hist);
         colst[(wv * R + r) * 32 + lane] = make_uint2(nst.cur, nst.first);
       }
-      // band column summary of column cfin (rows [i0, min(i_end, cfin)))
-      if (cfin < n && cfin > i0) {
-        // stored as (top run, bottom run): traversal was bottom-up
-        Cb[cfin - i0] = acc.uniform ? pack_col(acc.first, acc.first)
-                                    : pack_col(acc.last, acc.first);
-      } else if (cfin == i0) {
-        Cb[0] = 0u;
+      if (cfin < nrem) {
+        // column part of hook (i0 + cfin) inside this band: rows [i0, min(i_end, i0 + cfin))
+        Cb[cfin] = (cfin == 0) ? 0u
+                 : acc.uniform ? pack_col(acc.first, acc.first)
+                               : pack_col(acc.last, acc.first);  // (top, bottom)
       }
     }
     __syncthreads();
 
     // ---- slot R-1 leaves the band through its bottom edge
     {
-      const int64_t kd = kx - (int64_t)(R - 1) * HS + delta;
-      if (kd >= 0 && kd < nrem && i_end - 1 + kd < n) {
-        DiagRun& e = st[R - 1];
-        if (e.rooted) Pb[kd] = (uint16_t)e.len;
-        Sb[kd] = (uint16_t)e.len;
-      }
+      const int kd = kx - (R - 1) * HS + delta;
+      if (kd >= 0 && kd < nrem && kd < bot_rows)
+        diag_finish(st[R - 1], true, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
     }
     if (((x + 1) & 4095) == 0) {
-      __syncthreads();
       for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
         const uint32_t cnt = sh_hist[q];
         if (cnt) {
@@ -413,35 +416,35 @@ sym_kernel(const SymArgs a, const int W_rt) {
     }
   }
 
-  // ---- drain diagonal slots (all remaining cells are right of column n-1)
+  // ---- drain: slots still holding diagonals after the last iteration.  All
+  // their remaining cells lie right of column n-1: a segment with rows left
+  // in the band is cut there; otherwise it leaves through the bottom edge.
 #pragma unroll
   for (int dstep = 1; dstep < R; ++dstep) {
-    const int64_t kx = (X + dstep - 1) * D;
+    const int kx = (X + dstep - 1) * D;
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       if (r >= dstep) {
-        const int64_t kd = kx - (int64_t)r * HS + delta;
-        if (kd >= 0 && kd < nrem && i_end > i0 + (int64_t)r * HS && (st[r].len | st[r].rooted))
-          diag_end_run(st[r], Pb + kd, kd == 0 ? 1u : 2u, hist);
+        const int kd = kx - r * HS + delta;
+        if (kd >= 0 && kd < nrem && hrows > r * HS && st[r].cur != 0u) {
+          diag_finish(st[r], false, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
+          st[r] = RunState{1u, 0u};  // finished: nothing left to report
+        }
       }
     }
     {
-      const int64_t kd = kx - (int64_t)(R - 1) * HS + delta;
-      if (kd >= 0 && kd < nrem && i_end - 1 + kd < n) {
-        DiagRun& e = st[R - 1];
-        if (e.rooted) Pb[kd] = (uint16_t)e.len;
-        Sb[kd] = (uint16_t)e.len;
-      }
+      const int kd = kx - (R - 1) * HS + delta;
+      if (kd >= 0 && kd < nrem && kd < bot_rows && st[R - 1].cur != 0u)
+        diag_finish(st[R - 1], true, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
     }
 #pragma unroll
     for (int r = R - 1; r >= 1; --r) st[r] = st[r - 1];
-    st[0].len = 0;
-    st[0].rooted = 0;
+    st[0] = RunState{0u, 0u};
   }
 
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) pts += __shfl_xor_sync(0xffffffffu, pts, o);
-  if (lane == 0 && pts) atomicAdd(a.points, pts);
+  for (int o = 16; o >= 1; o >>= 1) pts64 += __shfl_xor_sync(0xffffffffu, pts64, o);
+  if (lane == 0 && pts64) atomicAdd(a.points, pts64);
   __syncthreads();
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
     const uint32_t cnt = sh_hist[q];
