@@ -108,6 +108,90 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
   st.cur = cur + (((uint32_t)nb - pos) << 1);
 }
 
+// ---------------------------------------------------------------------------
+// Deferred run emission.  A pass over one word per lane only updates the
+// lane's run state (branch-free); the runs the word closes are described by
+// an event (boundary mask + the carried run) pushed into a per-warp ring in
+// shared memory, and events are expanded 32 at a time, one per lane, so the
+// histogram updates run at full SIMD width even when only a few lanes of a
+// pass see a boundary.
+// ---------------------------------------------------------------------------
+constexpr int kQueueCap = 64;  // events per warp (uint4 each)
+
+// Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
+// bit 0 skip the carried run (it is the sequence's first run, kept in the
+// state), bits 1..2 diagonal weight (0: vertical/white sink).
+__device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
+  uint32_t bnd = e.x;
+  const uint32_t w = e.z >> 1;
+  uint32_t bit = e.y & 1u;
+  uint32_t len = e.y >> 1;        // carried length: added to the first closed run
+  uint32_t pos = 0;
+  bool skip = (e.z & 1u) != 0u;
+  while (bnd) {
+    const uint32_t p = (uint32_t)__ffs(bnd) - 1u;
+    const uint32_t l = len + (p - pos);
+    if (!skip) {
+      if (w == 0u) h.add(bit ? kVert : kWhite, l, 1u);
+      else if (bit) h.add(kDiag, l, w);
+    }
+    skip = false;
+    len = 0u;
+    bit ^= 1u;
+    pos = p;
+    bnd &= bnd - 1u;
+  }
+}
+
+struct EventQueue {
+  uint4* ring;     // this warp's kQueueCap entries
+  uint32_t head;   // warp-uniform
+  uint32_t tail;   // warp-uniform
+};
+
+__device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int lane, bool all) {
+  while (q.tail - q.head >= 32u || (all && q.tail != q.head)) {
+    const uint32_t avail = q.tail - q.head;
+    if ((uint32_t)lane < avail) expand_event(q.ring[(q.head + lane) % kQueueCap], h);
+    q.head += avail < 32u ? avail : 32u;
+  }
+  __syncwarp();
+}
+
+// One pass: consume nb (1..32) bits of x, bit 0 first, into the lane's run
+// state; closed runs go to the queue.  diag_weight 0: both run values count
+// (vertical / white vertical); 1 or 2: only runs of ones count as diagonal
+// lines with that weight.  All lanes of the warp must call it.
+__device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
+                                          EventQueue& q, const Hist& h, int lane) {
+  const uint32_t full = low_mask(nb);
+  x &= full;
+  uint32_t cur = st.cur;
+  if (cur == 0u) cur = x & 1u;                         // sequence starts here
+  const uint32_t bnd = (x ^ ((x << 1) | (cur & 1u))) & full;
+  const bool ev = (nb > 0) && (bnd != 0u);
+  uint4 e = make_uint4(bnd, cur, diag_weight << 1, 0u);
+  if (ev) {
+    const uint32_t plast = 31u - (uint32_t)__clz(bnd);
+    if (st.first == 0u) {                              // the carried run is the first run
+      const uint32_t p1 = (uint32_t)__ffs(bnd) - 1u;
+      st.first = cur + (p1 << 1);
+      e.z |= 1u;
+    }
+    cur = (((uint32_t)nb - plast) << 1) | ((x >> plast) & 1u);
+  } else if (nb > 0) {
+    cur += (uint32_t)nb << 1;
+  }
+  st.cur = cur;
+  const uint32_t m = __ballot_sync(0xffffffffu, ev);
+  if (ev) q.ring[(q.tail + __popc(m & ((1u << lane) - 1u))) % kQueueCap] = e;
+  q.tail += __popc(m);
+  if (q.tail - q.head >= 32u) {
+    __syncwarp();
+    queue_drain(q, h, lane, false);
+  }
+}
+
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {
   if (st.cur == 0u) return Seg{0u, 0u, 0u};
   if (st.first == 0u) return Seg{st.cur, st.cur, 1u};

@@ -49,7 +49,7 @@ __host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot
 
 struct SymSmem {
   int H, HS, D, W, CW;
-  size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_hist, total;
+  size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_queue, off_hist, total;
   __host__ __device__ SymSmem(int NW, int R, int W_) {
     D = 32 * NW;
     HS = D;
@@ -63,7 +63,8 @@ struct SymSmem {
     off_rowbuf = off_col1 + (size_t)CW * sizeof(double);
     off_prev = off_rowbuf + (size_t)NW * H * sizeof(uint32_t);
     off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
-    off_hist = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
+    off_queue = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
+    off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
     total = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;
   }
 };
@@ -135,6 +136,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
   uint32_t* lead_out = a.rowlead + i0;
   const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
   const Transposer tr(lane);
+  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u};
 
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
   for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
@@ -296,10 +298,11 @@ sym_kernel(const SymArgs a, const int W_rt) {
         // diagonal runs: bits [0, lc) are cells; the segment is cut by the
         // matrix's right edge in the chunk holding relative row lastc (unless
         // it runs down to the band's last row: openb)
-        if (kd >= 0 && kd < nrem) {
+        {
+          const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
-          if (rel > 0) runs_consume(word, min(rel, 32), st[r], LineSink{&hist, kd == 0 ? 1u : 2u});
-          if (!openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+          runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
+          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
             diag_finish(st[r], false, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
             st[r] = RunState{1u, 0u};  // finished: later slots of this diagonal are empty
           }
@@ -316,28 +319,23 @@ sym_kernel(const SymArgs a, const int W_rt) {
     for (int r = 0; r < R; ++r) {
       const int lr = r * HS + tid;
       prev_next[lr] = rowbuf[(NW - 1) * H + lr];
-      if (x >= r && lr < hrows) {
-        const int rem = nrem - lr - (x - r) * D;      // valid diagonals of this row from k0
+      const bool act = x >= r && lr < hrows;
+      const int rem = act ? nrem - lr - (x - r) * D : 0;  // valid diagonals of this row from k0
+      if (__any_sync(0xffffffffu, rem > 0)) {
+#pragma unroll 2
+        for (int v = 0; v < NW; ++v) {
+          const int nb = min(max(rem - 32 * v, 0), 32);
+          const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
+          pts += __popc(w);
+          runs_pass(w, nb, rs[r], 0u, evq, hist, lane);
+        }
         if (rem > 0) {
-          if (rem > D) {
-#pragma unroll 4
-            for (int v = 0; v < NW; ++v) {
-              const uint32_t w = rowbuf[v * H + lr];
-              pts += __popc(w);
-              runs_consume(w, 32, rs[r], vsink);
-            }
-          } else {
-            for (int v = 0; 32 * v < rem; ++v) {
-              const int nb = min(rem - 32 * v, 32);
-              const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
-              pts += __popc(w);
-              runs_consume(w, nb, rs[r], vsink);
-            }
-            const Seg sg = runs_finish(rs[r]);      // the row ends at column n-1
+          if (x == r) pts64 -= (rowbuf[lr] & 1u);      // the diagonal cell counts once
+          if (rem <= D) {                                // the row ends at column n-1
+            const Seg sg = runs_finish(rs[r]);
             lead_out[lr] = sg.first;
             if (!sg.uniform) emit_run(sg.last, hist);
           }
-          if (x == r) pts64 -= (rowbuf[lr] & 1u);      // the diagonal cell counts once
         }
       }
     }
@@ -367,11 +365,10 @@ sym_kernel(const SymArgs a, const int W_rt) {
             const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
             const int col = finishing ? cfin : cnew;
             const int lim = min(max(min(col, hrows) - (r * HS + 32 * c), 0), 32);
-            if (lim > 0 && col < nrem) {
-              const uint32_t bits = __brev(colw) >> (32 - lim);
-              if (finishing) runs_consume(bits, lim, fin, vsink);
-              else runs_consume(bits, lim, nst, vsink);
-            }
+            const int nb = (col < nrem) ? lim : 0;
+            const uint32_t bits = nb > 0 ? (__brev(colw) >> (32 - nb)) : 0u;
+            if (finishing) runs_pass(bits, nb, fin, 0u, evq, hist, lane);
+            else runs_pass(bits, nb, nst, 0u, evq, hist, lane);
           }
         }
         acc = seg_combine(acc, runs_finish(fin), hist);
@@ -442,6 +439,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
     st[0] = RunState{0u, 0u};
   }
 
+  queue_drain(evq, hist, lane, true);
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) pts64 += __shfl_xor_sync(0xffffffffu, pts64, o);
   if (lane == 0 && pts64) atomicAdd(a.points, pts64);
