@@ -73,9 +73,14 @@ def exchange(so, world, group=None):
                         torch.empty(world, n, dtype=so.suffix.dtype, device=dev),
                         torch.empty(world, 2 * n, dtype=so.col.dtype, device=dev),
                         so.rowlead)
-    dist.all_gather_into_tensor(out.prefix, so.prefix, group=group)
-    dist.all_gather_into_tensor(out.suffix, so.suffix, group=group)
-    dist.all_gather_into_tensor(out.col, so.col, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.prefix, so.prefix, group=group)
+        dist.all_gather_into_tensor(out.suffix, so.suffix, group=group)
+        dist.all_gather_into_tensor(out.col, so.col, group=group)
+    else:  # gloo (CPU tests): list form
+        dist.all_gather(list(out.prefix.unbind(0)), so.prefix, group=group)
+        dist.all_gather(list(out.suffix.unbind(0)), so.suffix, group=group)
+        dist.all_gather(list(out.col.unbind(0)), so.col, group=group)
     dist.all_reduce(out.rowlead, group=group)
     return out
 
