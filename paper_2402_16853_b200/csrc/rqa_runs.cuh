@@ -144,52 +144,57 @@ __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
 }
 
 struct EventQueue {
-  uint4* ring;     // this warp's kQueueCap entries
-  uint32_t head;   // warp-uniform
-  uint32_t tail;   // warp-uniform
+  uint4* ring;       // this warp's kQueueCap entries
+  uint32_t head;     // warp-uniform
+  uint32_t tail;     // warp-uniform
+  uint32_t lt_mask;  // (1 << lane) - 1
 };
 
-__device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int lane, bool all) {
-  while (q.tail - q.head >= 32u || (all && q.tail != q.head)) {
-    const uint32_t avail = q.tail - q.head;
-    if ((uint32_t)lane < avail) expand_event(q.ring[(q.head + lane) % kQueueCap], h);
-    q.head += avail < 32u ? avail : 32u;
+// Expand whole groups of 32 events (all = true: everything left).  Kept out
+// of line: it runs once per ~10 passes and would otherwise be inlined at
+// every pass site.
+static __device__ __noinline__ uint32_t queue_drain_impl(const uint4* ring, uint32_t head, uint32_t tail,
+                                                  uint32_t sh, unsigned long long* g,
+                                                  int64_t stride, int lane, bool all) {
+  const Hist h{sh, g, stride};
+  while (tail - head >= 32u || (all && tail != head)) {
+    const uint32_t avail = tail - head;
+    if ((uint32_t)lane < avail) expand_event(ring[(head + lane) % kQueueCap], h);
+    head += avail < 32u ? avail : 32u;
   }
   __syncwarp();
+  return head;
 }
 
-// One pass: consume nb (1..32) bits of x, bit 0 first, into the lane's run
+__device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int lane, bool all) {
+  __syncwarp();
+  q.head = queue_drain_impl(q.ring, q.head, q.tail, h.sh, h.g, h.stride, lane, all);
+}
+
+// One pass: consume nb (0..32) bits of x, bit 0 first, into the lane's run
 // state; closed runs go to the queue.  diag_weight 0: both run values count
 // (vertical / white vertical); 1 or 2: only runs of ones count as diagonal
-// lines with that weight.  All lanes of the warp must call it.
+// lines with that weight.  All lanes of the warp must call it (nb = 0 for
+// lanes with nothing to consume).  Branch-free except the queue drain.
 __device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
                                           EventQueue& q, const Hist& h, int lane) {
-  const uint32_t full = low_mask(nb);
+  const uint32_t full = (nb >= 32) ? 0xffffffffu : ((1u << nb) - 1u);
   x &= full;
-  uint32_t cur = st.cur;
-  if (cur == 0u) cur = x & 1u;                         // sequence starts here
-  const uint32_t bnd = (x ^ ((x << 1) | (cur & 1u))) & full;
-  const bool ev = (nb > 0) && (bnd != 0u);
-  uint4 e = make_uint4(bnd, cur, diag_weight << 1, 0u);
-  if (ev) {
-    const uint32_t plast = 31u - (uint32_t)__clz(bnd);
-    if (st.first == 0u) {                              // the carried run is the first run
-      const uint32_t p1 = (uint32_t)__ffs(bnd) - 1u;
-      st.first = cur + (p1 << 1);
-      e.z |= 1u;
-    }
-    cur = (((uint32_t)nb - plast) << 1) | ((x >> plast) & 1u);
-  } else if (nb > 0) {
-    cur += (uint32_t)nb << 1;
-  }
-  st.cur = cur;
+  const uint32_t cur = st.cur ? st.cur : (x & 1u);            // sequence starts here
+  const uint32_t bnd = (x ^ ((x << 1) | (cur & 1u))) & full;  // run boundaries
+  const bool ev = bnd != 0u;
+  const uint32_t plast = 31u - (uint32_t)__clz(bnd);           // last boundary
+  const uint32_t p1 = (uint32_t)__ffs(bnd) - 1u;               // first boundary
+  const bool mkfirst = ev && st.first == 0u;                   // carried run is the first run
+  const uint32_t cur_ev = (((uint32_t)nb - plast) << 1) | ((x >> (plast & 31u)) & 1u);
+  st.first = mkfirst ? cur + (p1 << 1) : st.first;
+  st.cur = ev ? cur_ev : cur + ((uint32_t)nb << 1);
   const uint32_t m = __ballot_sync(0xffffffffu, ev);
-  if (ev) q.ring[(q.tail + __popc(m & ((1u << lane) - 1u))) % kQueueCap] = e;
+  if (ev)
+    q.ring[(q.tail + __popc(m & q.lt_mask)) % kQueueCap] =
+        make_uint4(bnd, cur, (diag_weight << 1) | (mkfirst ? 1u : 0u), 0u);
   q.tail += __popc(m);
-  if (q.tail - q.head >= 32u) {
-    __syncwarp();
-    queue_drain(q, h, lane, false);
-  }
+  if (q.tail - q.head >= 32u) queue_drain(q, h, lane, false);
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {

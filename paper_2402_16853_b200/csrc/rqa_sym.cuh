@@ -49,7 +49,8 @@ __host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot
 
 struct SymSmem {
   int H, HS, D, W, CW;
-  size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_queue, off_hist, total;
+  size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_rowst, off_queue,
+      off_hist, total;
   __host__ __device__ SymSmem(int NW, int R, int W_) {
     D = 32 * NW;
     HS = D;
@@ -63,7 +64,8 @@ struct SymSmem {
     off_rowbuf = off_col1 + (size_t)CW * sizeof(double);
     off_prev = off_rowbuf + (size_t)NW * H * sizeof(uint32_t);
     off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
-    off_queue = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
+    off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
+    off_queue = off_rowst + (size_t)R * D * sizeof(uint2);
     off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
     total = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;
   }
@@ -112,6 +114,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
   uint32_t* rowbuf = reinterpret_cast<uint32_t*>(smem + L.off_rowbuf);
   uint32_t* prevbuf = reinterpret_cast<uint32_t*>(smem + L.off_prev);
   uint2* colst = reinterpret_cast<uint2*>(smem + L.off_colst);
+  uint2* rowst = reinterpret_cast<uint2*>(smem + L.off_rowst);  // row-part run state (first, cur)
   uint32_t* sh_hist = reinterpret_cast<uint32_t*>(smem + L.off_hist);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_hist + 3 * kSmemBins * sizeof(uint32_t));
 
@@ -136,12 +139,14 @@ sym_kernel(const SymArgs a, const int W_rt) {
   uint32_t* lead_out = a.rowlead + i0;
   const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
   const Transposer tr(lane);
-  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u};
+  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
+                 (1u << lane) - 1u};
 
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
   for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
   for (int q = tid; q < 2 * H; q += NW * 32) prevbuf[q] = 0u;
   for (int q = tid; q < NW * R * 32; q += NW * 32) colst[q] = make_uint2(0u, 0u);
+  for (int q = tid; q < R * D; q += NW * 32) rowst[q] = make_uint2(0u, 0u);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -166,9 +171,6 @@ sym_kernel(const SymArgs a, const int W_rt) {
     ph_hi[r] = 0u;
   }
   const LineSink vsink{&hist, 0u};
-  RunState rs[R];  // row part of hook (i0 + r*HS + tid)
-#pragma unroll
-  for (int r = 0; r < R; ++r) rs[r] = RunState{0u, 0u};
   uint32_t pts = 0;  // per-thread partial, flushed to 64 bits every iteration
 
   unsigned long long pts64 = 0;
@@ -315,28 +317,40 @@ sym_kernel(const SymArgs a, const int W_rt) {
     // ---- row phase: upper row i = i0 + r*HS + tid, diagonals (x-r)*D + [0, D)
     const uint32_t* prev_cur = prevbuf + buf * H;   // iteration x-1's warp NW-1 words
     uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const int lr = r * HS + tid;
       prev_next[lr] = rowbuf[(NW - 1) * H + lr];
       const bool act = x >= r && lr < hrows;
       const int rem = act ? nrem - lr - (x - r) * D : 0;  // valid diagonals of this row from k0
       if (__any_sync(0xffffffffu, rem > 0)) {
+        const uint2 rsv = rowst[lr];
+        RunState rs{rsv.x, rsv.y};
+        if (__all_sync(0xffffffffu, rem >= D)) {          // common case: 8 full words
 #pragma unroll 2
-        for (int v = 0; v < NW; ++v) {
-          const int nb = min(max(rem - 32 * v, 0), 32);
-          const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
-          pts += __popc(w);
-          runs_pass(w, nb, rs[r], 0u, evq, hist, lane);
+          for (int v = 0; v < NW; ++v) {
+            const uint32_t w = rowbuf[v * H + lr];
+            pts += __popc(w);
+            runs_pass(w, 32, rs, 0u, evq, hist, lane);
+          }
+        } else {
+#pragma unroll 1
+          for (int v = 0; v < NW; ++v) {
+            const int nb = min(max(rem - 32 * v, 0), 32);
+            const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
+            pts += __popc(w);
+            runs_pass(w, nb, rs, 0u, evq, hist, lane);
+          }
         }
         if (rem > 0) {
           if (x == r) pts64 -= (rowbuf[lr] & 1u);      // the diagonal cell counts once
           if (rem <= D) {                                // the row ends at column n-1
-            const Seg sg = runs_finish(rs[r]);
+            const Seg sg = runs_finish(rs);
             lead_out[lr] = sg.first;
             if (!sg.uniform) emit_run(sg.last, hist);
           }
         }
+        rowst[lr] = make_uint2(rs.first, rs.cur);
       }
     }
     pts64 += 2ull * pts;
@@ -349,27 +363,34 @@ sym_kernel(const SymArgs a, const int W_rt) {
       Seg acc{0u, 0u, 0u};
       const int cfin = kx + 32 * wv + lane;      // finishing column, relative to i0
       const int cnew = cfin + D;                  // starting column
-#pragma unroll
+#pragma unroll 1
       for (int rr = 0; rr < R; ++rr) {
         const int r = R - 1 - rr;
-        uint2 cs = colst[(wv * R + r) * 32 + lane];
+        const uint2 cs = colst[(wv * R + r) * 32 + lane];
         RunState fin{cs.y, cs.x};
         RunState nst{0u, 0u};
         if (x >= r) {
+          // rows of slot r above each column (relative to the slot's first row)
+          const int lim_fin = (cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
+          const int lim_new = (cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
+          RunState cur{0u, 0u};
+#pragma unroll 1
           for (int c = NCH - 1; c >= 0; --c) {
+            if (c == wv) {                          // switch to the finishing column
+              nst = cur;
+              cur = fin;
+            }
             const bool finishing = c <= wv;
-            const int wp = finishing ? wv - c : wv + NW - c;
+            const int wp = (wv - c) & (NW - 1);
             const int lr = r * HS + 32 * c + lane;
             const uint32_t w1 = rowbuf[wp * H + lr];
             const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lr] : prev_cur[lr];
             const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
-            const int col = finishing ? cfin : cnew;
-            const int lim = min(max(min(col, hrows) - (r * HS + 32 * c), 0), 32);
-            const int nb = (col < nrem) ? lim : 0;
-            const uint32_t bits = nb > 0 ? (__brev(colw) >> (32 - nb)) : 0u;
-            if (finishing) runs_pass(bits, nb, fin, 0u, evq, hist, lane);
-            else runs_pass(bits, nb, nst, 0u, evq, hist, lane);
+            const int nb = min(max((finishing ? lim_fin : lim_new) - 32 * c, 0), 32);
+            const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
+            runs_pass(bits, nb, cur, 0u, evq, hist, lane);
           }
+          fin = cur;
         }
         acc = seg_combine(acc, runs_finish(fin), hist);
         colst[(wv * R + r) * 32 + lane] = make_uint2(nst.cur, nst.first);
