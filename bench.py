@@ -207,7 +207,7 @@ def main():
     so = StripeOutputs.empty(n, dev) if world > 1 else None
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    bounds = stripe_bounds(n, world, band_rows(settings))
+    bounds = stripe_bounds(n, world, band_rows(settings, n))
     lo, hi = bounds[rank], bounds[rank + 1]
 
     def step():

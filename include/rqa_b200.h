@@ -59,8 +59,9 @@ int64_t rqa_launch_counter(void);
  * for L2 with m > 1 (replaces sqrt, embedding.py:154-156), radius otherwise. */
 int rqa_threshold(int32_t metric, int32_t m, double radius, double *thr);
 
-/* Band height (rows per CTA) and kernel variant chosen for (metric, m, tau). */
-int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t *band_rows,
+/* Band height (rows per CTA) and kernel variant chosen for (metric, m, tau)
+ * and n embedded vectors (mid-size n uses shorter bands to balance the SMs). */
+int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t *band_rows,
                   int32_t *reuse_kernel);
 
 /*

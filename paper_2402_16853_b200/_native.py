@@ -28,7 +28,7 @@ SYMBOLS = {
     "rqa_device_count": (_c.c_int, []),
     "rqa_launch_counter": (_i64, []),
     "rqa_threshold": (_c.c_int, [_i32, _i32, _dbl, _pd]),
-    "rqa_band_rows": (_c.c_int, [_i32, _i32, _i32, _pi64, _pi32]),
+    "rqa_band_rows": (_c.c_int, [_i32, _i32, _i32, _i64, _pi64, _pi32]),
     "rqa_run": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _pi64, _pi64,
                            _pi64, _pi64, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_run_device": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _dbl, _i64, _i64, _i64, _i32,

@@ -119,7 +119,7 @@ int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
   p->radius = radius;
   p->thr = threshold_for(metric, m, radius);
   p->theiler = theiler;
-  if (!find_variant(metric, m, tau, &p->var))
+  if (!find_variant(metric, m, tau, p->n, &p->var))
     return set_err(err, errlen, "embedding window (m-1)*tau = %lld too large (max 4096)",
                    (long long)span),
            RQA_EINVAL;
@@ -256,10 +256,11 @@ int rqa_threshold(int32_t metric, int32_t m, double radius, double* thr) {
   return RQA_OK;
 }
 
-int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t* band_rows,
+int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t* band_rows,
                   int32_t* reuse_kernel) {
   Variant v;
-  if (m < 1 || tau < 1 || metric < 0 || metric > 2 || !find_variant(metric, m, tau, &v))
+  if (m < 1 || tau < 1 || metric < 0 || metric > 2 || n < 1 ||
+      !find_variant(metric, m, tau, n, &v))
     return RQA_EINVAL;
   if (band_rows) *band_rows = v.band_rows();
   if (reuse_kernel) *reuse_kernel = v.reuse;

@@ -94,8 +94,8 @@ __device__ __forceinline__ void diag_finish(const RunState& st, bool open, uint1
   }
 }
 
-template <int METRIC, int M, int TAU, int NW, int R>
-__global__ void __launch_bounds__(NW * 32, 2)
+template <int METRIC, int M, int TAU, int NW, int R, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
 sym_kernel(const SymArgs a, const int W_rt) {
   constexpr int D = 32 * NW;
   constexpr int HS = D;
@@ -105,7 +105,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
   constexpr bool kLinfAnd = (METRIC == kLinf) && (M >= 2);
   constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
   constexpr int NCH = HS / 32;  // == NW
-  static_assert(kW <= 32, "term window too large");
+  static_assert(kLinfAnd ? kW <= 32 : kW <= 48, "term window too large");
   const int W = kDirect ? W_rt : kW;
   const SymSmem L(NW, R, W);
 

@@ -13,10 +13,16 @@ struct Variant {
   int64_t band_rows() const { return (int64_t)r * 32 * nw; }
 };
 
+// 2 CTAs per SM, except the one-slot large-window variants (registers).
+template <int M, int TAU, int R>
+constexpr int min_blocks() {
+  return (R == 1 && M > 0 && (M - 1) * TAU > 16) ? 1 : (R == 2 ? 4 : 2);
+}
+
 template <int METRIC, int M, int TAU, int NW, int R>
 cudaError_t launch_sym(const SymArgs& a, int nbands, int w, cudaStream_t st) {
   const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
-  auto k = sym_kernel<METRIC, M, TAU, NW, R>;
+  auto k = sym_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, R>()>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   k<<<nbands, NW * 32, L.total, st>>>(a, w);
@@ -30,21 +36,27 @@ Variant make_variant(int w_rt) {
   return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_sym<METRIC, M, TAU, NW, R>};
 }
 
-// Implemented in rqa_kernels_<metric>.cu (one translation unit per metric so
-// the instantiations compile in parallel).
-bool find_variant_l1(int m, int tau, Variant* out);
-bool find_variant_l2(int m, int tau, Variant* out);
-bool find_variant_linf(int m, int tau, Variant* out);
-bool find_variant_m1(int m, int tau, Variant* out);
-bool find_variant_direct(int metric, int m, int tau, Variant* out);
+// Implemented in rqa_kernels_<metric>[_small].cu (one translation unit each so
+// the instantiations compile in parallel).  `small` selects the 256-row band
+// geometry (NW = 4, R = 2) used when the 1024-row bands would be too few to
+// balance the SMs (the upper triangle makes early bands the largest).
+bool find_variant_l1(int m, int tau, bool small, Variant* out);
+bool find_variant_l2(int m, int tau, bool small, Variant* out);
+bool find_variant_linf(int m, int tau, bool small, Variant* out);
+bool find_variant_m1(int m, int tau, bool small, Variant* out);
+bool find_variant_direct(int metric, int m, int tau, bool small, Variant* out);
 
-inline bool find_variant(int metric, int m, int tau, Variant* out) {
-  if (m == 1) return find_variant_m1(m, tau, out);
+// Rows of the matrix below which the 256-row geometry is chosen.
+constexpr int64_t kSmallGeometryBelow = 600000;
+
+inline bool find_variant(int metric, int m, int tau, int64_t n, Variant* out) {
+  const bool small = n < kSmallGeometryBelow;
+  if (m == 1) return find_variant_m1(m, tau, small, out);
   bool ok = false;
-  if (metric == kL1) ok = find_variant_l1(m, tau, out);
-  else if (metric == kL2) ok = find_variant_l2(m, tau, out);
-  else if (metric == kLinf) ok = find_variant_linf(m, tau, out);
-  return ok || find_variant_direct(metric, m, tau, out);
+  if (metric == kL1) ok = find_variant_l1(m, tau, small, out);
+  else if (metric == kL2) ok = find_variant_l2(m, tau, small, out);
+  else if (metric == kLinf) ok = find_variant_linf(m, tau, small, out);
+  return ok || find_variant_direct(metric, m, tau, small, out);
 }
 
 }  // namespace rqa

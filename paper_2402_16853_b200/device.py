@@ -17,12 +17,12 @@ MODE_FINAL = 0
 MODE_STRIPE = 1
 
 
-def band_rows(settings: AnalysisSettings) -> int:
-    """Rows per CTA band of the kernel variant chosen for these settings."""
+def band_rows(settings: AnalysisSettings, n: int) -> int:
+    """Rows per CTA band of the kernel variant chosen for these settings and n vectors."""
     h = ctypes.c_int64()
     r = ctypes.c_int32()
     rc = _native.lib().rqa_band_rows(METRIC_CODES[settings.metric], settings.embedding_dimension,
-                                     settings.time_delay, ctypes.byref(h), ctypes.byref(r))
+                                     settings.time_delay, int(n), ctypes.byref(h), ctypes.byref(r))
     if rc != 0:
         raise ValueError("no kernel variant for these settings")
     return int(h.value)

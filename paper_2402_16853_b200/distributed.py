@@ -108,7 +108,7 @@ def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSetting
     if band is None:
         from .device import band_rows
 
-        band = band_rows(settings)
+        band = band_rows(settings, n)
     bounds = stripe_bounds(n, world, band)
     series = torch.from_numpy(np.ascontiguousarray(embedded.values, np.float64)).to(device)
     hist, points, so = stripe_fn(series, settings, bounds[rank], bounds[rank + 1], n, device)

@@ -82,10 +82,15 @@ def test_band_rows():
     h = ctypes.c_int64()
     r = ctypes.c_int32()
     lib = _native.lib()
-    assert lib.rqa_band_rows(1, 3, 1, ctypes.byref(h), ctypes.byref(r)) == 0
-    assert h.value % 32 == 0 and r.value == 1
-    assert lib.rqa_band_rows(0, 10, 5, ctypes.byref(h), ctypes.byref(r)) == 0
-    assert lib.rqa_band_rows(5, 3, 1, ctypes.byref(h), ctypes.byref(r)) != 0
+    assert lib.rqa_band_rows(1, 3, 1, 1 << 20, ctypes.byref(h), ctypes.byref(r)) == 0
+    assert h.value == 1024 and r.value == 1
+    assert lib.rqa_band_rows(1, 3, 1, 100000, ctypes.byref(h), ctypes.byref(r)) == 0
+    assert h.value == 256 and r.value == 1            # mid-size n: shorter bands
+    assert lib.rqa_band_rows(0, 10, 5, 500000, ctypes.byref(h), ctypes.byref(r)) == 0
+    assert r.value == 1                               # C4 has a reuse variant
+    assert lib.rqa_band_rows(0, 17, 3, 500000, ctypes.byref(h), ctypes.byref(r)) == 0
+    assert r.value == 0                               # runtime (m, tau) kernel
+    assert lib.rqa_band_rows(5, 3, 1, 1000, ctypes.byref(h), ctypes.byref(r)) != 0
 
 
 def test_invalid_arguments_map_to_reference_errors():

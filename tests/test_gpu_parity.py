@@ -177,7 +177,7 @@ def test_stripes_then_stitch_equal_single_run():
         ref_h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
         ref_p = torch.zeros(1, dtype=torch.int64, device=dev)
         run_rows_device(sd, st, 0, n, MODE_FINAL, ref_h, ref_p)
-        band = band_rows(st)
+        band = band_rows(st, n)
         for g in (1, 2, 3, 5):
             bounds = stripe_bounds(n, g, band)
             h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
