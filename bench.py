@@ -189,13 +189,20 @@ def main():
     from paper_2402_16853_b200 import _native, embed, run_analysis
     from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, StripeOutputs, band_rows,
                                               run_rows_device, stitch_device)
-    from paper_2402_16853_b200.distributed import exchange, stripe_bounds
+    from paper_2402_16853_b200.distributed import all_reduce, exchange, reduce_sum, stripe_bounds
 
+    # RQA_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo
+    shared = os.environ.get("RQA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = _native.lib()
@@ -220,8 +227,8 @@ def main():
             run_rows_device(series, settings, lo, hi, MODE_STRIPE, hist, points, so,
                             stream=stream)
             gathered = exchange(so, world)
-            dist.reduce(hist, dst=0)
-            dist.reduce(points, dst=0)
+            reduce_sum(hist, 0)
+            reduce_sum(points, 0)
             if rank == 0:
                 stitch_device(gathered, bounds, n, hist)
 
@@ -250,7 +257,7 @@ def main():
     t_step = float(np.mean(times))
     if world > 1:
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step = float(tt.item())
     cells = float(n) * float(n)
     value = cells / t_step

@@ -60,6 +60,33 @@ def gpu_stitch_fn(gathered, bounds, n, hist):
     stitch_device(gathered, bounds, n, hist)
 
 
+def _gloo_staged(fn, *tensors):
+    """Run a gloo collective on CPU copies of CUDA tensors (test setups only)."""
+    host = [t.cpu() for t in tensors]
+    fn(*host)
+    for t, h in zip(tensors, host):
+        t.copy_(h)
+
+
+def reduce_sum(t, dst=0, group=None):
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" or not t.is_cuda:
+        dist.reduce(t, dst=dst, group=group)
+    else:
+        _gloo_staged(lambda h: dist.reduce(h, dst=dst, group=group), t)
+
+
+def all_reduce(t, op=None, group=None):
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if dist.get_backend(group) == "nccl" or not t.is_cuda:
+        dist.all_reduce(t, op=op, group=group)
+    else:
+        _gloo_staged(lambda h: dist.all_reduce(h, op=op, group=group), t)
+
+
 def exchange(so, world, group=None):
     """All-gather the stripe edge summaries, sum the row leads (disjoint rows)."""
     import torch
@@ -77,11 +104,12 @@ def exchange(so, world, group=None):
         dist.all_gather_into_tensor(out.prefix, so.prefix, group=group)
         dist.all_gather_into_tensor(out.suffix, so.suffix, group=group)
         dist.all_gather_into_tensor(out.col, so.col, group=group)
-    else:  # gloo (CPU tests): list form
-        dist.all_gather(list(out.prefix.unbind(0)), so.prefix, group=group)
-        dist.all_gather(list(out.suffix.unbind(0)), so.suffix, group=group)
-        dist.all_gather(list(out.col.unbind(0)), so.col, group=group)
-    dist.all_reduce(out.rowlead, group=group)
+    else:  # gloo (CPU tests / shared-GPU test runs): list form on host copies
+        for dst, src in ((out.prefix, so.prefix), (out.suffix, so.suffix), (out.col, so.col)):
+            parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, src.cpu(), group=group)
+            dst.copy_(torch.stack(parts))
+    all_reduce(out.rowlead, group=group)
     return out
 
 
@@ -113,8 +141,8 @@ def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSetting
     series = torch.from_numpy(np.ascontiguousarray(embedded.values, np.float64)).to(device)
     hist, points, so = stripe_fn(series, settings, bounds[rank], bounds[rank + 1], n, device)
     gathered = exchange(so, world, group)
-    dist.reduce(hist, dst=0, group=group)
-    dist.reduce(points, dst=0, group=group)
+    reduce_sum(hist, 0, group)
+    reduce_sum(points, 0, group)
     if rank != 0:
         return None
     stitch_fn(gathered, bounds, n, hist)
