@@ -116,30 +116,45 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 // histogram updates run at full SIMD width even when only a few lanes of a
 // pass see a boundary.
 // ---------------------------------------------------------------------------
-constexpr int kQueueCap = 64;  // events per warp (uint4 each)
+constexpr int kQueueCap = 64;  // events per warp (uint4 each); drained at >= 32
 
 // Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
 // bit 0 skip the carried run (it is the sequence's first run, kept in the
 // state), bits 1..2 diagonal weight (0: vertical/white sink).
+__device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint32_t len,
+                                         uint32_t w) {
+  // len < kSmemBins: 32-bit shared bin; else 64-bit global counter
+  const uint32_t sa = h.sh + 4u * (kind_row * (uint32_t)kSmemBins + len);
+  unsigned long long* ga = h.g + (int64_t)kind_row * h.stride + len;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.lt.u32 p, %0, %4;\n\t"
+      "@p red.shared.add.u32 [%1], %3;\n\t"
+      "@!p red.global.add.u64 [%2], %5;\n\t}" ::"r"(len),
+      "r"(sa), "l"(ga), "r"(w), "n"(kSmemBins), "l"((unsigned long long)w)
+      : "memory");
+}
+
 __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
   uint32_t bnd = e.x;
   const uint32_t w = e.z >> 1;
+  // weight and histogram row of runs of zeroes / ones
+  const uint32_t w0 = (w == 0u) ? 1u : 0u, w1 = (w == 0u) ? 1u : w;
+  const uint32_t k0 = kWhite, k1 = (w == 0u) ? (uint32_t)kVert : (uint32_t)kDiag;
   uint32_t bit = e.y & 1u;
-  uint32_t len = e.y >> 1;        // carried length: added to the first closed run
-  uint32_t pos = 0;
-  bool skip = (e.z & 1u) != 0u;
-  while (bnd) {
-    const uint32_t p = (uint32_t)__ffs(bnd) - 1u;
-    const uint32_t l = len + (p - pos);
-    if (!skip) {
-      if (w == 0u) h.add(bit ? kVert : kWhite, l, 1u);
-      else if (bit) h.add(kDiag, l, w);
-    }
-    skip = false;
-    len = 0u;
-    bit ^= 1u;
-    pos = p;
+  // first closed run: carried length + first boundary position
+  uint32_t p = (uint32_t)__ffs(bnd) - 1u;
+  uint32_t len = (e.y >> 1) + p;
+  uint32_t wt = (e.z & 1u) ? 0u : (bit ? w1 : w0);
+  for (;;) {
+    if (wt) hist_red(h, bit ? k1 : k0, len, wt);
     bnd &= bnd - 1u;
+    if (bnd == 0u) break;
+    const uint32_t q = (uint32_t)__ffs(bnd) - 1u;
+    len = q - p;
+    p = q;
+    bit ^= 1u;
+    wt = bit ? w1 : w0;
   }
 }
 
@@ -172,12 +187,13 @@ __device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int la
 }
 
 // One pass: consume nb (0..32) bits of x, bit 0 first, into the lane's run
-// state; closed runs go to the queue.  diag_weight 0: both run values count
-// (vertical / white vertical); 1 or 2: only runs of ones count as diagonal
-// lines with that weight.  All lanes of the warp must call it (nb = 0 for
-// lanes with nothing to consume).  Branch-free except the queue drain.
-__device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
-                                          EventQueue& q, const Hist& h, int lane) {
+// state; closed runs go to the queue (no drain: the caller drains, the ring
+// holds kQueueCap events).  diag_weight 0: both run values count (vertical /
+// white vertical); 1 or 2: only runs of ones count as diagonal lines with
+// that weight.  All lanes of the warp must call it (nb = 0 for lanes with
+// nothing to consume).  Branch-free.
+__device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
+                                          EventQueue& q) {
   const uint32_t full = (nb >= 32) ? 0xffffffffu : ((1u << nb) - 1u);
   x &= full;
   const uint32_t cur = st.cur ? st.cur : (x & 1u);            // sequence starts here
@@ -194,6 +210,11 @@ __device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint
     q.ring[(q.tail + __popc(m & q.lt_mask)) % kQueueCap] =
         make_uint4(bnd, cur, (diag_weight << 1) | (mkfirst ? 1u : 0u), 0u);
   q.tail += __popc(m);
+}
+
+__device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
+                                          EventQueue& q, const Hist& h, int lane) {
+  runs_push(x, nb, st, diag_weight, q);
   if (q.tail - q.head >= 32u) queue_drain(q, h, lane, false);
 }
 

@@ -226,6 +226,38 @@ sym_kernel(const SymArgs a, const int W_rt) {
       openb[r] = (crows == vrows) ? 1 : 0;
     }
 
+    // Bookkeeping of one finished chunk cc (its R words): diagonal runs,
+    // row words to shared memory.  Software-pipelined: chunk c-1 is booked
+    // inside the same basic block as chunk c's FP64 steps so the scheduler
+    // can overlap the integer work with the FP64 pipe.
+    auto book = [&](int cc, const uint32_t (&words)[R], bool valid) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int kd = kdr[r];
+        const bool live = valid && kd >= 0 && kd < nrem;
+        const int rel = lastc[r] - 32 * cc;
+        runs_pass(words[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
+                  lane);
+        const uint32_t rw = tr(words[r]);
+        if (valid) rowbuf[wv * H + r * HS + 32 * cc + lane] = rw;
+      }
+    };
+    // the segment of slot r is cut by the matrix's right edge in this chunk
+    auto close_cut = [&](int cc) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int kd = kdr[r];
+        const int rel = lastc[r] - 32 * cc;
+        if (kd >= 0 && kd < nrem && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+          diag_finish(st[r], false, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
+          st[r] = RunState{1u, 0u};  // finished: later slots of this diagonal are empty
+        }
+      }
+    };
+
+    uint32_t pw[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) pw[r] = 0u;
     for (int c = 0; c < NCH; ++c) {
       uint32_t dw[R];
 #pragma unroll
@@ -282,7 +314,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
           }
         }
       }
-
+      // finalise this chunk's words (Linf AND of shifted predicates, Theiler band)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         uint32_t word;
@@ -295,22 +327,11 @@ sym_kernel(const SymArgs a, const int W_rt) {
         } else {
           word = dw[r];
         }
-        const int kd = kdr[r];
-        if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-        // diagonal runs: bits [0, lc) are cells; the segment is cut by the
-        // matrix's right edge in the chunk holding relative row lastc (unless
-        // it runs down to the band's last row: openb)
-        {
-          const bool live = kd >= 0 && kd < nrem;
-          const int rel = lastc[r] - 32 * c;
-          runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
-          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
-            diag_finish(st[r], false, Pb + kd, Sb + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
-            st[r] = RunState{1u, 0u};  // finished: later slots of this diagonal are empty
-          }
-        }
-        rowbuf[wv * H + r * HS + 32 * c + lane] = tr(word);
+        pw[r] = (kdr[r] < theiler) ? 0u : word;  // also the lower triangle kd < 0
       }
+      book(c, pw, true);
+      close_cut(c);
+      if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
     }
     __syncthreads();
 

@@ -1,5 +1,7 @@
 // rqa_variants.cuh -- compile-time kernel variants and their launchers.
 #pragma once
+#include <cstdlib>
+
 #include "rqa_sym.cuh"
 
 namespace rqa {
@@ -50,7 +52,11 @@ bool find_variant_direct(int metric, int m, int tau, bool small, Variant* out);
 constexpr int64_t kSmallGeometryBelow = 600000;
 
 inline bool find_variant(int metric, int m, int tau, int64_t n, Variant* out) {
-  const bool small = n < kSmallGeometryBelow;
+  // RQA_GEOMETRY=small|big overrides the choice (benchmarking / tests)
+  static const char* force = getenv("RQA_GEOMETRY");
+  const bool small = force && force[0] == 's' ? true
+                   : force && force[0] == 'b' ? false
+                                              : n < kSmallGeometryBelow;
   if (m == 1) return find_variant_m1(m, tau, small, out);
   bool ok = false;
   if (metric == kL1) ok = find_variant_l1(m, tau, small, out);
