@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -185,7 +186,24 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.rowlead = rowlead;
   a.hist = hist;
   a.points = points;
+  static const char* skip_env = getenv("RQA_SKIP");  // profiling only: skip phases
+  a.skip = skip_env ? atoi(skip_env) : 0;
+  static const bool timers = getenv("RQA_TIMERS") != nullptr;  // profiling only: phase cycles
+  a.timers = nullptr;
+  if (timers) {
+    RQA_CUDA(cudaMalloc(&a.timers, 4 * sizeof(unsigned long long)), "timers");
+    RQA_CUDA(cudaMemsetAsync(a.timers, 0, 4 * sizeof(unsigned long long), st), "timers");
+  }
   RQA_CUDA(p.var.launch(a, (int)nb, p.var.w, st), "launching band kernel");
+  if (timers) {
+    unsigned long long t[4];
+    RQA_CUDA(cudaMemcpyAsync(t, a.timers, sizeof t, cudaMemcpyDeviceToHost, st), "timers");
+    RQA_CUDA(cudaStreamSynchronize(st), "timers");
+    const double tot = (double)(t[0] + t[1] + t[2] + t[3]);
+    fprintf(stderr, "phase cycles (warp-summed): compute %.3f rows %.3f cols %.3f other %.3f\n",
+            t[0] / tot, t[1] / tot, t[2] / tot, t[3] / tot);
+    cudaFree(a.timers);
+  }
   g_launches++;
   if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
 

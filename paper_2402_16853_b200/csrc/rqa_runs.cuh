@@ -116,7 +116,7 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 // histogram updates run at full SIMD width even when only a few lanes of a
 // pass see a boundary.
 // ---------------------------------------------------------------------------
-constexpr int kQueueCap = 64;  // events per warp (uint4 each); drained at >= 32
+constexpr int kQueueCap = 128;  // events per warp (uint4 each); drained at >= 32
 
 // Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
 // bit 0 skip the carried run (it is the sequence's first run, kept in the

@@ -34,6 +34,8 @@ struct SymArgs {
   uint32_t* rowlead;         // [n]: first run of upper row i from the diagonal
   unsigned long long* hist;  // [3][n+1]
   unsigned long long* points;
+  int skip;                  // profiling only (RQA_SKIP): 1 diag runs, 2 row phase, 4 column phase
+  unsigned long long* timers;  // profiling only (RQA_TIMERS): [4] cycles compute/rows/cols/other
 };
 
 // Compact per-band offset of entries kd (or c - i0) in [0, n - i0).
@@ -161,6 +163,9 @@ sym_kernel(const SymArgs a, const int W_rt) {
     tma_load_1d(smem + L.off_col0, src, col_bytes, &bar[0]);
   }
 
+  // profiling experiment: offset CTAs so co-resident CTAs are out of phase
+  if (a.skip & 8) { if ((blockIdx.x & 1) && tid == 0) __nanosleep(13000); __syncthreads(); }
+  if (a.skip & 16) { if (((blockIdx.x / 148) & 1) && tid == 0) __nanosleep(13000); __syncthreads(); }
   RunState st[R];  // diagonal run state per slot (first run = band-top run)
   double win[R][kW > 0 ? kW : 1];
   uint32_t ph_lo[R], ph_hi[R];
@@ -174,6 +179,8 @@ sym_kernel(const SymArgs a, const int W_rt) {
   uint32_t pts = 0;  // per-thread partial, flushed to 64 bits every iteration
 
   unsigned long long pts64 = 0;
+  unsigned long long tm[4] = {0, 0, 0, 0};
+  long long tprev = clock64();
   for (int x = 0; x < X; ++x) {
     const int kx = x * D;
     const int buf = x & 1;
@@ -236,8 +243,9 @@ sym_kernel(const SymArgs a, const int W_rt) {
         const int kd = kdr[r];
         const bool live = valid && kd >= 0 && kd < nrem;
         const int rel = lastc[r] - 32 * cc;
-        runs_pass(words[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
-                  lane);
+        if (!(a.skip & 1))
+          runs_pass(words[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq,
+                    hist, lane);
         const uint32_t rw = tr(words[r]);
         if (valid) rowbuf[wv * H + r * HS + 32 * cc + lane] = rw;
       }
@@ -335,86 +343,131 @@ sym_kernel(const SymArgs a, const int W_rt) {
     }
     __syncthreads();
 
+    if (a.timers) { const long long t = clock64(); tm[0] += t - tprev; tprev = t; }
     // ---- row phase: upper row i = i0 + r*HS + tid, diagonals (x-r)*D + [0, D)
     const uint32_t* prev_cur = prevbuf + buf * H;   // iteration x-1's warp NW-1 words
     uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
+    // two slots per pass: their run chains are independent (ILP)
+    constexpr int PR = (R % 2 == 0) ? 2 : 1;
 #pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-      const int lr = r * HS + tid;
-      prev_next[lr] = rowbuf[(NW - 1) * H + lr];
-      const bool act = x >= r && lr < hrows;
-      const int rem = act ? nrem - lr - (x - r) * D : 0;  // valid diagonals of this row from k0
-      if (__any_sync(0xffffffffu, rem > 0)) {
-        const uint2 rsv = rowst[lr];
-        RunState rs{rsv.x, rsv.y};
-        if (__all_sync(0xffffffffu, rem >= D)) {          // common case: 8 full words
+    for (int r0 = 0; r0 < R; r0 += PR) {
+      int lr[PR], rem[PR];
+      RunState rs[PR];
+      bool any_rem = false, all_full = true;
+#pragma unroll
+      for (int p = 0; p < PR; ++p) {
+        const int r = r0 + p;
+        lr[p] = r * HS + tid;
+        prev_next[lr[p]] = rowbuf[(NW - 1) * H + lr[p]];
+        const bool act = x >= r && lr[p] < hrows;
+        rem[p] = act ? nrem - lr[p] - (x - r) * D : 0;  // valid diagonals of this row from k0
+        any_rem |= rem[p] > 0;
+        all_full &= rem[p] >= D;
+      }
+      if (!(a.skip & 2) && __any_sync(0xffffffffu, any_rem)) {
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const uint2 rsv = rowst[lr[p]];
+          rs[p] = RunState{rsv.x, rsv.y};
+        }
+        if (__all_sync(0xffffffffu, all_full)) {          // common case: full words
 #pragma unroll 2
           for (int v = 0; v < NW; ++v) {
-            const uint32_t w = rowbuf[v * H + lr];
-            pts += __popc(w);
-            runs_pass(w, 32, rs, 0u, evq, hist, lane);
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const uint32_t w = rowbuf[v * H + lr[p]];
+              pts += __popc(w);
+              runs_push(w, 32, rs[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
           }
         } else {
 #pragma unroll 1
           for (int v = 0; v < NW; ++v) {
-            const int nb = min(max(rem - 32 * v, 0), 32);
-            const uint32_t w = rowbuf[v * H + lr] & low_mask(nb);
-            pts += __popc(w);
-            runs_pass(w, nb, rs, 0u, evq, hist, lane);
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const int nb = min(max(rem[p] - 32 * v, 0), 32);
+              const uint32_t w = rowbuf[v * H + lr[p]] & low_mask(nb);
+              pts += __popc(w);
+              runs_push(w, nb, rs[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
           }
         }
-        if (rem > 0) {
-          if (x == r) pts64 -= (rowbuf[lr] & 1u);      // the diagonal cell counts once
-          if (rem <= D) {                                // the row ends at column n-1
-            const Seg sg = runs_finish(rs);
-            lead_out[lr] = sg.first;
-            if (!sg.uniform) emit_run(sg.last, hist);
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const int r = r0 + p;
+          if (rem[p] > 0) {
+            if (x == r) pts64 -= (rowbuf[lr[p]] & 1u);   // the diagonal cell counts once
+            if (rem[p] <= D) {                             // the row ends at column n-1
+              const Seg sg = runs_finish(rs[p]);
+              lead_out[lr[p]] = sg.first;
+              if (!sg.uniform) emit_run(sg.last, hist);
+            }
           }
+          rowst[lr[p]] = make_uint2(rs[p].first, rs[p].cur);
         }
-        rowst[lr] = make_uint2(rs.first, rs.cur);
       }
     }
     pts64 += 2ull * pts;
     pts = 0;
+    if (a.timers) { const long long t = clock64(); tm[1] += t - tprev; tprev = t; }
 
     // ---- column phase: warp wv finishes column block u = wv (chunks wv..0)
     // and starts block u = wv + NW (chunks NW-1..wv+1) of every slot; lane =
-    // column; rows are consumed bottom-up.
+    // column; rows are consumed bottom-up; two slots per pass (ILP).
     {
       Seg acc{0u, 0u, 0u};
       const int cfin = kx + 32 * wv + lane;      // finishing column, relative to i0
       const int cnew = cfin + D;                  // starting column
 #pragma unroll 1
-      for (int rr = 0; rr < R; ++rr) {
-        const int r = R - 1 - rr;
-        const uint2 cs = colst[(wv * R + r) * 32 + lane];
-        RunState fin{cs.y, cs.x};
-        RunState nst{0u, 0u};
-        if (x >= r) {
+      for (int rr0 = 0; rr0 < R; rr0 += PR) {
+        int rs_[PR], lim_fin[PR], lim_new[PR];
+        RunState cur[PR], nst[PR], fin[PR];
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const int r = R - 1 - (rr0 + p);        // bottom-up over slots
+          rs_[p] = r;
+          const uint2 cs = colst[(wv * R + r) * 32 + lane];
+          fin[p] = RunState{cs.y, cs.x};
+          nst[p] = RunState{0u, 0u};
+          cur[p] = RunState{0u, 0u};
           // rows of slot r above each column (relative to the slot's first row)
-          const int lim_fin = (cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
-          const int lim_new = (cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
-          RunState cur{0u, 0u};
+          lim_fin[p] = (x >= r && cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
+          lim_new[p] = (x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
+        }
+        if (!(a.skip & 4) && x >= rs_[PR - 1]) {   // the lower slot index is active last
 #pragma unroll 1
           for (int c = NCH - 1; c >= 0; --c) {
-            if (c == wv) {                          // switch to the finishing column
-              nst = cur;
-              cur = fin;
+            if (c == wv) {                          // switch to the finishing columns
+#pragma unroll
+              for (int p = 0; p < PR; ++p) {
+                nst[p] = cur[p];
+                cur[p] = fin[p];
+              }
             }
             const bool finishing = c <= wv;
             const int wp = (wv - c) & (NW - 1);
-            const int lr = r * HS + 32 * c + lane;
-            const uint32_t w1 = rowbuf[wp * H + lr];
-            const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lr] : prev_cur[lr];
-            const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
-            const int nb = min(max((finishing ? lim_fin : lim_new) - 32 * c, 0), 32);
-            const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
-            runs_pass(bits, nb, cur, 0u, evq, hist, lane);
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const int lr = rs_[p] * HS + 32 * c + lane;
+              const uint32_t w1 = rowbuf[wp * H + lr];
+              const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lr] : prev_cur[lr];
+              const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
+              const int nb = min(max((finishing ? lim_fin[p] : lim_new[p]) - 32 * c, 0), 32);
+              const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
+              runs_push(bits, nb, cur[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
           }
-          fin = cur;
+#pragma unroll
+          for (int p = 0; p < PR; ++p) fin[p] = cur[p];
         }
-        acc = seg_combine(acc, runs_finish(fin), hist);
-        colst[(wv * R + r) * 32 + lane] = make_uint2(nst.cur, nst.first);
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          acc = seg_combine(acc, runs_finish(fin[p]), hist);
+          colst[(wv * R + rs_[p]) * 32 + lane] = make_uint2(nst[p].cur, nst[p].first);
+        }
       }
       if (cfin < nrem) {
         // column part of hook (i0 + cfin) inside this band: rows [i0, min(i_end, i0 + cfin))
@@ -425,6 +478,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
     }
     __syncthreads();
 
+    if (a.timers) { const long long t = clock64(); tm[2] += t - tprev; tprev = t; }
     // ---- slot R-1 leaves the band through its bottom edge
     {
       const int kd = kx - (R - 1) * HS + delta;
@@ -482,6 +536,11 @@ sym_kernel(const SymArgs a, const int W_rt) {
   }
 
   queue_drain(evq, hist, lane, true);
+  if (a.timers && lane == 0) {
+    const long long t = clock64();
+    tm[3] += t - tprev;
+    for (int k = 0; k < 4; ++k) atomicAdd(&a.timers[k], tm[k]);
+  }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) pts64 += __shfl_xor_sync(0xffffffffu, pts64, o);
   if (lane == 0 && pts64) atomicAdd(a.points, pts64);

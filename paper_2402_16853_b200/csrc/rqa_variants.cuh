@@ -16,15 +16,15 @@ struct Variant {
 };
 
 // 2 CTAs per SM, except the one-slot large-window variants (registers).
-template <int M, int TAU, int R>
+template <int M, int TAU, int NW, int R>
 constexpr int min_blocks() {
-  return (R == 1 && M > 0 && (M - 1) * TAU > 16) ? 1 : (R == 2 ? 4 : 2);
+  return (R == 1 && M > 0 && (M - 1) * TAU > 16) ? 1 : (NW == 4 ? 4 : (R == 2 ? 3 : 2));
 }
 
 template <int METRIC, int M, int TAU, int NW, int R>
 cudaError_t launch_sym(const SymArgs& a, int nbands, int w, cudaStream_t st) {
   const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
-  auto k = sym_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, R>()>;
+  auto k = sym_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   k<<<nbands, NW * 32, L.total, st>>>(a, w);
@@ -56,7 +56,13 @@ inline bool find_variant(int metric, int m, int tau, int64_t n, Variant* out) {
   static const char* force = getenv("RQA_GEOMETRY");
   const bool small = force && force[0] == 's' ? true
                    : force && force[0] == 'b' ? false
+                   : force && force[0] == 'm' ? false
                                               : n < kSmallGeometryBelow;
+  if (force && force[0] == 'm' && metric == kL2 && m == 3 && tau == 1) {  // experiment
+    extern Variant mid_variant_l2_3_1();
+    *out = mid_variant_l2_3_1();
+    return true;
+  }
   if (m == 1) return find_variant_m1(m, tau, small, out);
   bool ok = false;
   if (metric == kL1) ok = find_variant_l1(m, tau, small, out);
