@@ -22,5 +22,6 @@ bool find_variant_l2(int m, int tau, bool small, Variant* out) {
 }
 
 Variant mid_variant_l2_3_1() { return make_variant<kL2, 3, 1, 8, 2>(0); }
+Variant pipe_variant_l2_3_1() { return make_pipe_variant<kL2, 3, 1, 8, 2>(0); }
 
 }  // namespace rqa

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdlib>
 
+#include "rqa_pipe.cuh"
 #include "rqa_sym.cuh"
 
 namespace rqa {
@@ -38,6 +39,24 @@ Variant make_variant(int w_rt) {
   return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_sym<METRIC, M, TAU, NW, R>};
 }
 
+template <int METRIC, int M, int TAU, int NW, int R>
+cudaError_t launch_pipe(const SymArgs& a, int nbands, int w, cudaStream_t st) {
+  const PipeSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
+  auto k = pipe_kernel<METRIC, M, TAU, NW, R, 2>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  k<<<nbands, NW * 32, L.total, st>>>(a, w);
+  return cudaGetLastError();
+}
+
+template <int METRIC, int M, int TAU, int NW, int R>
+Variant make_pipe_variant(int w_rt) {
+  static_assert(R <= 2, "the pipelined kernel's event ring holds 3*R*32 events per chunk");
+  const int w = (M == 0) ? w_rt : (M - 1) * TAU;
+  const PipeSmem L(NW, R, w);
+  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_pipe<METRIC, M, TAU, NW, R>};
+}
+
 // Implemented in rqa_kernels_<metric>[_small].cu (one translation unit each so
 // the instantiations compile in parallel).  `small` selects the 256-row band
 // geometry (NW = 4, R = 2) used when the 1024-row bands would be too few to
@@ -56,11 +75,16 @@ inline bool find_variant(int metric, int m, int tau, int64_t n, Variant* out) {
   static const char* force = getenv("RQA_GEOMETRY");
   const bool small = force && force[0] == 's' ? true
                    : force && force[0] == 'b' ? false
-                   : force && force[0] == 'm' ? false
+                   : force && (force[0] == 'm' || force[0] == 'p') ? false
                                               : n < kSmallGeometryBelow;
   if (force && force[0] == 'm' && metric == kL2 && m == 3 && tau == 1) {  // experiment
     extern Variant mid_variant_l2_3_1();
     *out = mid_variant_l2_3_1();
+    return true;
+  }
+  if (force && force[0] == 'p' && metric == kL2 && m == 3 && tau == 1) {  // experiment
+    extern Variant pipe_variant_l2_3_1();
+    *out = pipe_variant_l2_3_1();
     return true;
   }
   if (m == 1) return find_variant_m1(m, tau, small, out);
