@@ -42,7 +42,8 @@ extern "C" {
 /* Number of timing slots written by rqa_run (seconds):
  * [0] h2d, [1] band kernel, [2] fold kernel, [3] d2h, [4] total device span,
  * [5] cells per second over the band+fold kernels, [6] band height,
- * [7] number of bands. */
+ * [7] number of bands.  Very large n is split into row stripes processed
+ * one after the other on the device when the band summaries would not fit. */
 #define RQA_TIMING_SLOTS 8
 
 /* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
@@ -85,8 +86,9 @@ int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t m
  *       d_stripe_col (uint32[2n]): per column c the first and last run
  *         ((len << 1) | bit) of the column's part inside the stripe above the
  *         main diagonal;
- *       d_rowlead (uint32[n], zero-initialised by the caller): for the
- *         stripe's rows i, the first run of row i right of the diagonal.
+ *       d_rowpart (uint32[2n], zero-initialised by the caller): for the
+ *         stripe's rows i, the first and last run of row i from the diagonal
+ *         to column n-1.
  *     All four go to rqa_stitch_device (after an all-gather / sum-reduce).
  * Only the upper triangle k >= 0 is evaluated: R = R^T exactly, so diagonal
  * -k equals diagonal k and column c equals the "hook" (upper column c above
@@ -97,19 +99,19 @@ int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t m
 int rqa_run_device(const double *d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                    double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
                    int64_t *d_hist, int64_t *d_points, int32_t *d_stripe_prefix,
-                   int32_t *d_stripe_suffix, uint32_t *d_stripe_col, uint32_t *d_rowlead,
+                   int32_t *d_stripe_suffix, uint32_t *d_stripe_col, uint32_t *d_rowpart,
                    void *stream, char *err, size_t errlen);
 
 /*
  * Cross-stripe stitch (engine.py:287-319 carry contract + flush :195-212):
  * d_prefix / d_suffix (int32[nstripes][n]) and d_col (uint32[nstripes][2n])
- * gathered from every stripe in row order, d_rowlead (uint32[n]) summed over
+ * gathered from every stripe in row order, d_rowpart (uint32[2n]) summed over
  * the stripes, bounds (host) the nstripes+1 stripe row boundaries.  Adds the
  * diagonal, vertical and white-vertical lines that cross stripe edges into
  * d_hist.
  */
 int rqa_stitch_device(const int32_t *d_prefix, const int32_t *d_suffix, const uint32_t *d_col,
-                      const uint32_t *d_rowlead, const int64_t *bounds, int32_t nstripes,
+                      const uint32_t *d_rowpart, const int64_t *bounds, int32_t nstripes,
                       int64_t n, int64_t *d_hist, void *stream, char *err, size_t errlen);
 
 /* FP64 pipe microbenchmark on `device`: sustained DADD and DMUL operations

@@ -56,8 +56,18 @@ struct Workspace {
   size_t ps_cap = 0;  // elements
   uint32_t* cs = nullptr;      // column-part summaries (compact band layout)
   size_t cs_cap = 0;
-  uint32_t* rowlead = nullptr; // [n]
+  uint32_t* rowlead = nullptr; // [2n] row part per row (single-device final mode)
   size_t rowlead_cap = 0;
+  uint2* rowpiece = nullptr;   // [nunits][H]
+  size_t rowpiece_cap = 0;
+  Unit* units = nullptr;       // [nunits] launch order
+  size_t units_cap = 0;
+  int4* units_bb = nullptr;    // [nunits] sorted by band, xa
+  size_t units_bb_cap = 0;
+  int32_t* band_start = nullptr;
+  size_t band_start_cap = 0;
+  int32_t* stripe_buf = nullptr;  // auto-striping: [G][n] x2 + [G][2n] + [2n]
+  size_t stripe_buf_cap = 0;
   unsigned long long* hist = nullptr;
   size_t hist_cap = 0;  // elements (3*(n+1) + 1 for points)
   int64_t* bounds = nullptr;
@@ -126,6 +136,7 @@ int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
            RQA_EINVAL;
   const int64_t H = p->var.band_rows(), D = 32 * p->var.nw;
   p->pad = 2 * H + 4 * D + p->var.w + 256;
+  (void)D;
   return RQA_OK;
 }
 
@@ -153,24 +164,100 @@ int stage_series(Workspace* ws, const Problem& p, const double* src, cudaMemcpyK
   return RQA_OK;
 }
 
-// Upper-triangle band kernel over rows [row_lo, row_hi) + folds.
+// Work units: every band's diagonal sweep is cut into iteration ranges of
+// about `len` iterations so that the grid has several waves of similar CTAs
+// (the upper triangle makes the first bands the longest).
+struct UnitPlan {
+  std::vector<Unit> units;       // launch order (longest first)
+  std::vector<int4> by_band;     // (band, xa, xb, idx) sorted by band, xa
+  std::vector<int32_t> band_start;
+};
+
+UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots) {
+  const int64_t H = p.var.band_rows(), D = p.var.slot_rows(), R = p.var.r;
+  const int64_t nb = (row_hi - row_lo + H - 1) / H;
+  std::vector<int64_t> X(nb);
+  int64_t total = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t nrem = p.n - (row_lo + b * H);
+    X[b] = (nrem + D - 1) / D + R - 1;
+    total += X[b];
+  }
+  // aim for >= 4 waves of units; one recomputed iteration per unit boundary
+  int64_t len = std::max<int64_t>(8, total / std::max<int64_t>(1, 4LL * slots));
+  UnitPlan pl;
+  pl.band_start.assign(nb + 1, 0);
+  for (int64_t b = 0; b < nb; ++b) {
+    pl.band_start[b] = (int32_t)pl.by_band.size();
+    const int64_t parts = std::max<int64_t>(1, (X[b] + len - 1) / len);
+    for (int64_t q = 0; q < parts; ++q) {
+      const int32_t xa = (int32_t)(X[b] * q / parts), xb = (int32_t)(X[b] * (q + 1) / parts);
+      const int32_t idx = (int32_t)pl.units.size();
+      pl.units.push_back(Unit{(int32_t)b, xa, xb, idx});
+      pl.by_band.push_back(make_int4((int)b, xa, xb, idx));
+    }
+  }
+  pl.band_start[nb] = (int32_t)pl.by_band.size();
+  std::stable_sort(pl.units.begin(), pl.units.end(),
+                   [](const Unit& u, const Unit& v) { return (u.xb - u.xa) > (v.xb - v.xa); });
+  return pl;
+}
+
+int64_t unit_workspace_bytes(const Problem& p, int64_t row_lo, int64_t row_hi) {
+  const int64_t H = p.var.band_rows(), HS = p.var.slot_rows();
+  const int64_t nb = (row_hi - row_lo + H - 1) / H;
+  const int64_t nslots = (row_hi - row_lo + HS - 1) / HS;
+  return 2 * slot_offset(nslots, p.n, row_lo, HS) * 2 + sym_band_offset(nb, p.n, row_lo, H) * 4;
+}
+
+// Work-unit kernel over rows [row_lo, row_hi) + folds.
 //   final mode: diagonal and hook folds write the complete histograms;
-//   stripe mode: per-stripe summaries for rqa_stitch_device (multi-GPU).
+//   stripe mode: per-stripe summaries for the cross-stripe stitch.
 int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi, int mode,
                 unsigned long long* hist, unsigned long long* points, int32_t* out_p,
-                int32_t* out_s, uint32_t* out_col, uint32_t* rowlead, cudaStream_t st,
+                int32_t* out_s, uint32_t* out_col, uint32_t* out_row, cudaStream_t st,
                 cudaEvent_t ev_mid, char* err, size_t errlen) {
-  const int64_t H = p.var.band_rows();
+  const int64_t H = p.var.band_rows(), HS = p.var.slot_rows();
   const int64_t nb = (row_hi - row_lo + H - 1) / H;
   if (nb <= 0) return RQA_OK;
-  const int64_t total = sym_band_offset(nb, p.n, row_lo, H);  // compact entries
-  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * total)), "allocating band summaries");
-  RQA_CUDA(grow(&ws->cs, &ws->cs_cap, (size_t)total), "allocating column summaries");
-  if (!rowlead) {
-    RQA_CUDA(grow(&ws->rowlead, &ws->rowlead_cap, (size_t)p.n), "allocating row leads");
-    rowlead = ws->rowlead;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  RQA_CUDA(cudaFuncSetAttribute(p.var.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p.var.smem),
+           "kernel attributes");
+  RQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.var.kernel, 32 * p.var.nw,
+                                                         p.var.smem),
+           "occupancy");
+  const UnitPlan pl = plan_units(p, row_lo, row_hi, sms * std::max(1, per_sm));
+  const int64_t nunits = (int64_t)pl.units.size();
+  const int64_t nslots = (row_hi - row_lo + HS - 1) / HS;
+  const int64_t ptot = slot_offset(nslots, p.n, row_lo, HS);
+  const int64_t ctot = sym_band_offset(nb, p.n, row_lo, H);
+  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * ptot)), "allocating diagonal summaries");
+  RQA_CUDA(grow(&ws->cs, &ws->cs_cap, (size_t)ctot), "allocating column summaries");
+  RQA_CUDA(grow(&ws->rowpiece, &ws->rowpiece_cap, (size_t)(nunits * H)), "allocating row pieces");
+  RQA_CUDA(grow(&ws->units, &ws->units_cap, (size_t)nunits), "allocating units");
+  RQA_CUDA(grow(&ws->units_bb, &ws->units_bb_cap, (size_t)nunits), "allocating units");
+  RQA_CUDA(grow(&ws->band_start, &ws->band_start_cap, (size_t)nb + 1), "allocating units");
+  RQA_CUDA(cudaMemcpyAsync(ws->units, pl.units.data(), nunits * sizeof(Unit),
+                           cudaMemcpyHostToDevice, st),
+           "copying units");
+  RQA_CUDA(cudaMemcpyAsync(ws->units_bb, pl.by_band.data(), nunits * sizeof(int4),
+                           cudaMemcpyHostToDevice, st),
+           "copying units");
+  RQA_CUDA(cudaMemcpyAsync(ws->band_start, pl.band_start.data(), (nb + 1) * sizeof(int32_t),
+                           cudaMemcpyHostToDevice, st),
+           "copying units");
+  uint32_t* rowpart = out_row;
+  if (!rowpart) {  // final mode: the hook fold does not need a separate row-part array
+    RQA_CUDA(grow(&ws->rowlead, &ws->rowlead_cap, (size_t)(2 * p.n)), "allocating row parts");
+    rowpart = ws->rowlead;
   }
-  SymArgs a;
+
+  UnitArgs ua;
+  memset(&ua, 0, sizeof ua);
+  SymArgs& a = ua.base;
   a.s = ws->s_pad + p.pad;
   a.len = p.len;
   a.n = p.n;
@@ -180,56 +267,126 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.theiler = p.theiler;
   a.m = p.m;
   a.tau = p.tau;
-  a.P = ws->ps;
-  a.S = ws->ps + total;
+  a.P = ws->ps;               // [2][ptot]: P then S, per-slot compact layout
+  a.S = ws->ps + ptot;
   a.colsum = ws->cs;
-  a.rowlead = rowlead;
+  a.rowlead = nullptr;
   a.hist = hist;
   a.points = points;
   static const char* skip_env = getenv("RQA_SKIP");  // profiling only: skip phases
   a.skip = skip_env ? atoi(skip_env) : 0;
-  static const bool timers = getenv("RQA_TIMERS") != nullptr;  // profiling only: phase cycles
   a.timers = nullptr;
-  if (timers) {
-    RQA_CUDA(cudaMalloc(&a.timers, 4 * sizeof(unsigned long long)), "timers");
-    RQA_CUDA(cudaMemsetAsync(a.timers, 0, 4 * sizeof(unsigned long long), st), "timers");
-  }
-  RQA_CUDA(p.var.launch(a, (int)nb, p.var.w, st), "launching band kernel");
-  if (timers) {
-    unsigned long long t[4];
-    RQA_CUDA(cudaMemcpyAsync(t, a.timers, sizeof t, cudaMemcpyDeviceToHost, st), "timers");
-    RQA_CUDA(cudaStreamSynchronize(st), "timers");
-    const double tot = (double)(t[0] + t[1] + t[2] + t[3]);
-    fprintf(stderr, "phase cycles (warp-summed): compute %.3f rows %.3f cols %.3f other %.3f\n",
-            t[0] / tot, t[1] / tot, t[2] / tot, t[3] / tot);
-    cudaFree(a.timers);
-  }
+  ua.units = ws->units;
+  ua.rowpiece = ws->rowpiece;
+  RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
   g_launches++;
   if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
 
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((p.n + threads - 1) / threads, 148 * 16);
   SymFoldArgs f;
   memset(&f, 0, sizeof f);
   f.P = a.P;
   f.S = a.S;
-  f.colsum = a.colsum;
   f.row_lo = row_lo;
   f.row_hi = row_hi;
-  f.H = H;
-  f.nb = (int)nb;
-  f.rowlead = rowlead;
+  f.H = HS;                   // diagonal segments are slots
+  f.nb = (int)nslots;
   f.n = p.n;
   f.hist = hist;
   f.out_p = out_p;
   f.out_s = out_s;
-  f.out_col = reinterpret_cast<uint2*>(out_col);
-  const int threads = 256;
-  const int64_t blocks = std::min<int64_t>((p.n + threads - 1) / threads, 148 * 16);
   sym_fold_diag<<<(int)blocks, threads, 0, st>>>(f, mode);
   RQA_CUDA(cudaGetLastError(), "launching diagonal fold");
-  sym_fold_hooks<<<(int)blocks, threads, 0, st>>>(f, mode);
+  UnitFoldArgs h;
+  memset(&h, 0, sizeof h);
+  h.colsum = ws->cs;
+  h.rowpiece = ws->rowpiece;
+  h.units_by_band = ws->units_bb;
+  h.band_start = ws->band_start;
+  h.row_lo = row_lo;
+  h.row_hi = row_hi;
+  h.H = H;
+  h.HS = HS;
+  h.D = p.var.slot_rows();
+  h.nb = (int)nb;
+  h.n = p.n;
+  h.hist = hist;
+  h.out_col = reinterpret_cast<uint2*>(out_col);
+  h.out_row = reinterpret_cast<uint2*>(rowpart);
+  unit_fold_hooks<<<(int)blocks, threads, 0, st>>>(h, mode);
   RQA_CUDA(cudaGetLastError(), "launching hook fold");
   g_launches += 2;
   return RQA_OK;
+}
+
+int stitch_stripes(Workspace* ws, const int32_t* d_prefix, const int32_t* d_suffix,
+                   const uint32_t* d_col, const uint32_t* d_row, const int64_t* bounds,
+                   int32_t nstripes, int64_t n, unsigned long long* hist, cudaStream_t st,
+                   char* err, size_t errlen) {
+  RQA_CUDA(grow(&ws->bounds, &ws->bounds_cap, (size_t)nstripes + 1), "allocating bounds");
+  RQA_CUDA(cudaMemcpyAsync(ws->bounds, bounds, (nstripes + 1) * sizeof(int64_t),
+                           cudaMemcpyHostToDevice, st),
+           "copying bounds");
+  UnitStitchArgs f;
+  f.sp = d_prefix;
+  f.ss = d_suffix;
+  f.scol = reinterpret_cast<const uint2*>(d_col);
+  f.srow = reinterpret_cast<const uint2*>(d_row);
+  f.bounds = ws->bounds;
+  f.nseg = nstripes;
+  f.n = n;
+  f.hist = hist;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+  unit_fold_stripes<<<(int)blocks, threads, 0, st>>>(f);
+  RQA_CUDA(cudaGetLastError(), "launching stitch kernel");
+  g_launches++;
+  return RQA_OK;
+}
+
+// Equal-area row stripes of the upper triangle, band aligned.
+std::vector<int64_t> area_stripes(int64_t n, int g, int64_t band) {
+  std::vector<int64_t> b(1, 0);
+  for (int q = 1; q < g; ++q) {
+    const double i = (double)n * (1.0 - std::sqrt(1.0 - (double)q / g));
+    int64_t v = (int64_t)std::llround(i / band) * band;
+    b.push_back(std::max(b.back(), std::min(n, v)));
+  }
+  b.push_back(n);
+  return b;
+}
+
+// Full analysis on the current device; splits into sequential stripes (same
+// code path as multi-GPU) when the summaries would not fit in memory.
+int run_full(Workspace* ws, const Problem& p, unsigned long long* hist, unsigned long long* points,
+             cudaStream_t st, cudaEvent_t ev_mid, char* err, size_t errlen) {
+  size_t free_b = 0, total_b = 0;
+  RQA_CUDA(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  const double budget = 0.6 * (double)(free_b + ws->ps_cap * 2 + ws->cs_cap * 4);
+  const double need = (double)unit_workspace_bytes(p, 0, p.n);
+  int g = 1;
+  while (need / g > budget && g < 64) g *= 2;
+  if (g == 1)
+    return launch_rows(ws, p, 0, p.n, kFoldFinal, hist, points, nullptr, nullptr, nullptr, nullptr,
+                       st, ev_mid, err, errlen);
+  const std::vector<int64_t> bounds = area_stripes(p.n, g, p.var.band_rows());
+  const size_t per = (size_t)p.n;
+  RQA_CUDA(grow(&ws->stripe_buf, &ws->stripe_buf_cap, (size_t)g * per * 4 + 2 * per),
+           "allocating stripe summaries");
+  int32_t* pre = ws->stripe_buf;
+  int32_t* suf = pre + (size_t)g * per;
+  uint32_t* col = reinterpret_cast<uint32_t*>(suf + (size_t)g * per);
+  uint32_t* row = col + (size_t)g * 2 * per;
+  RQA_CUDA(cudaMemsetAsync(row, 0, 2 * per * sizeof(uint32_t), st), "memset row parts");
+  for (int q = 0; q < g; ++q) {
+    const int rc = launch_rows(ws, p, bounds[q], bounds[q + 1], kFoldStripe, hist, points,
+                               pre + (size_t)q * per, suf + (size_t)q * per,
+                               col + (size_t)q * 2 * per, row, st, nullptr, err, errlen);
+    if (rc) return rc;
+  }
+  if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
+  return stitch_stripes(ws, pre, suf, col, row, bounds.data(), g, p.n, hist, st, err, errlen);
 }
 
 // FP64 pipe microbenchmark: 8 independent DADD (or DMUL) chains per thread.
@@ -313,8 +470,7 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
   if (rc) return rc;
   RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 1) * sizeof(unsigned long long), st), "memset");
   RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
-  rc = launch_rows(ws, p, 0, p.n, kFoldFinal, ws->hist, ws->hist + 3 * hn, nullptr, nullptr,
-                   nullptr, nullptr, st, ws->ev[2], err, errlen);
+  rc = run_full(ws, p, ws->hist, ws->hist + 3 * hn, st, ws->ev[2], err, errlen);
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[3], st), "event");
   RQA_CUDA(cudaMemcpyAsync(diag, ws->hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
@@ -371,16 +527,18 @@ int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, 
   if (rc) return rc;
   const size_t hn = (size_t)(p.n + 1);
   (void)hn;
+  if (mode == kFoldFinal)
+    return run_full(ws, p, reinterpret_cast<unsigned long long*>(d_hist),
+                    reinterpret_cast<unsigned long long*>(d_points), st, nullptr, err, errlen);
   return launch_rows(ws, p, row_lo, row_hi, mode, reinterpret_cast<unsigned long long*>(d_hist),
                      reinterpret_cast<unsigned long long*>(d_points), d_stripe_prefix,
-                     d_stripe_suffix, mode == kFoldStripe ? d_stripe_col : nullptr,
-                     mode == kFoldStripe ? d_rowlead : nullptr, st, nullptr, err, errlen);
+                     d_stripe_suffix, d_stripe_col, d_rowlead, st, nullptr, err, errlen);
 }
 
 int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const uint32_t* d_col,
-                      const uint32_t* d_rowlead, const int64_t* bounds, int32_t nstripes, int64_t n,
-                      int64_t* d_hist, void* stream, char* err, size_t errlen) {
-  if (!d_prefix || !d_suffix || !d_col || !d_rowlead || !bounds || !d_hist || nstripes < 1 || n < 1)
+                      const uint32_t* d_rowpart, const int64_t* bounds, int32_t nstripes,
+                      int64_t n, int64_t* d_hist, void* stream, char* err, size_t errlen) {
+  if (!d_prefix || !d_suffix || !d_col || !d_rowpart || !bounds || !d_hist || nstripes < 1 || n < 1)
     return set_err(err, errlen, "invalid stitch arguments"), RQA_EINVAL;
   if (bounds[0] != 0 || bounds[nstripes] != n)
     return set_err(err, errlen, "stripes must cover rows [0, n)"), RQA_EINVAL;
@@ -392,25 +550,9 @@ int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const ui
   Workspace* ws = workspace(dev);
   std::lock_guard<std::mutex> lk(ws->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  RQA_CUDA(grow(&ws->bounds, &ws->bounds_cap, (size_t)nstripes + 1), "allocating bounds");
-  RQA_CUDA(cudaMemcpyAsync(ws->bounds, bounds, (nstripes + 1) * sizeof(int64_t),
-                           cudaMemcpyHostToDevice, st),
-           "copying bounds");
-  SymFoldArgs f;
-  memset(&f, 0, sizeof f);
-  f.sp = d_prefix;
-  f.ss = d_suffix;
-  f.scol = reinterpret_cast<const uint2*>(d_col);
-  f.bounds = ws->bounds;
-  f.nseg = nstripes;
-  f.rowlead = d_rowlead;
-  f.n = n;
-  f.hist = reinterpret_cast<unsigned long long*>(d_hist);
-  const int threads = 256;
-  const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
-  sym_fold_stripes<<<(int)blocks, threads, 0, st>>>(f);
-  RQA_CUDA(cudaGetLastError(), "launching stitch kernel");
-  g_launches++;
+  const int rc = stitch_stripes(ws, d_prefix, d_suffix, d_col, d_rowpart, bounds, nstripes, n,
+                                reinterpret_cast<unsigned long long*>(d_hist), st, err, errlen);
+  if (rc) return rc;
   RQA_CUDA(cudaStreamSynchronize(st), "stitch");
   return RQA_OK;
 }
@@ -460,6 +602,11 @@ int rqa_release(void) {
     cudaFree(ws->ps);
     cudaFree(ws->cs);
     cudaFree(ws->rowlead);
+    cudaFree(ws->rowpiece);
+    cudaFree(ws->units);
+    cudaFree(ws->units_bb);
+    cudaFree(ws->band_start);
+    cudaFree(ws->stripe_buf);
     cudaFree(ws->hist);
     cudaFree(ws->bounds);
     if (ws->init) {

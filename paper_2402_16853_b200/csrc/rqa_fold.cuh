@@ -242,3 +242,122 @@ __global__ void sym_fold_stripes(const SymFoldArgs a) {
 }
 
 }  // namespace rqa
+
+// ===========================================================================
+// Folds of the work-unit kernel (rqa_unit.cuh).  Diagonals use sym_fold_diag
+// with per-slot segments (H := HS); hooks combine the per-band column parts
+// with the per-unit row pieces of the row's own band.
+// ===========================================================================
+namespace rqa {
+
+struct UnitFoldArgs {
+  const uint32_t* colsum;      // compact per band (height H)
+  const uint2* rowpiece;       // [nunits][H]
+  const int4* units_by_band;   // (band, xa, xb, idx) sorted by band then xa
+  const int32_t* band_start;   // [nb+1] into units_by_band
+  int64_t row_lo, row_hi, H, HS, D;
+  int nb;
+  int64_t n;
+  unsigned long long* hist;
+  uint2* out_col;              // stripe mode: column part per c
+  uint2* out_row;              // stripe mode: row part per row (rows of the stripe)
+};
+
+__global__ void unit_fold_hooks(const UnitFoldArgs a, const int mode) {
+  const int64_t n = a.n;
+  const GHist h{a.hist, n + 1};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    // column part: bands above row c
+    Seg acc{0u, 0u, 0u};
+    for (int g = 0; g < a.nb; ++g) {
+      const int64_t lo = a.row_lo + g * a.H;
+      if (lo >= c) break;
+      const int64_t hi = min(lo + a.H, a.row_hi);
+      const int64_t L = min(hi, c) - lo;
+      const uint32_t v = a.colsum[sym_band_offset(g, n, a.row_lo, a.H) + (c - lo)];
+      const uint32_t top = v >> 16, bot = v & 0xffffu;
+      acc = seg_combine(acc, Seg{top, bot, (int64_t)run_len(top) == L ? 1u : 0u}, h);
+    }
+    // row part: pieces of row c (only if the row belongs to these bands)
+    Seg row{0u, 0u, 0u};
+    if (c >= a.row_lo && c < a.row_hi) {
+      const int64_t rel = c - a.row_lo;
+      const int bc = (int)(rel / a.H);
+      const int64_t lr = rel - (int64_t)bc * a.H;
+      const int r = (int)(lr / a.HS);
+      const int64_t rows = n - c;  // row part: diagonals [0, n-c)
+      for (int q = a.band_start[bc]; q < a.band_start[bc + 1]; ++q) {
+        const int4 u = a.units_by_band[q];
+        const int64_t k0 = max((int64_t)(u.y - r) * a.D, (int64_t)0);
+        const int64_t k1 = min((int64_t)(u.z - r) * a.D, rows);
+        if (k1 <= k0) continue;
+        const uint2 p = a.rowpiece[(int64_t)u.w * a.H + lr];
+        row = seg_combine(row, Seg{p.x, p.y, (int64_t)run_len(p.x) == k1 - k0 ? 1u : 0u}, h);
+      }
+    }
+    if (mode == kFoldFinal) {
+      seg_flush(seg_combine(acc, row, h), h);
+    } else {
+      a.out_col[c] = make_uint2(acc.first, acc.last);
+      if (c >= a.row_lo && c < a.row_hi) a.out_row[c] = make_uint2(row.first, row.last);
+    }
+  }
+}
+
+// Final fold over stripes (multi-GPU) for the work-unit layout.
+struct UnitStitchArgs {
+  const int32_t* sp;        // [nseg][n] diagonal prefix
+  const int32_t* ss;        // [nseg][n] diagonal suffix
+  const uint2* scol;        // [nseg][n] column part per stripe
+  const uint2* srow;        // [n] row part (each row from its own stripe)
+  const int64_t* bounds;    // nseg+1
+  int nseg;
+  int64_t n;
+  unsigned long long* hist;
+};
+
+__global__ void unit_fold_stripes(const UnitStitchArgs a) {
+  const int64_t n = a.n;
+  const GHist h{a.hist, n + 1};
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    {
+      const unsigned long long wgt = (k == 0) ? 1ull : 2ull;
+      const int64_t rows = n - k;
+      int64_t open = 0;
+      for (int g = 0; g < a.nseg; ++g) {
+        const int64_t lo = a.bounds[g], hi = a.bounds[g + 1];
+        if (lo >= rows) break;
+        if (hi <= lo) continue;
+        const int64_t L = min(hi, rows) - lo;
+        const int64_t p = a.sp[g * n + k];
+        if (p == L) {
+          open += L;
+          continue;
+        }
+        const int64_t x = open + p;
+        if (x > 0) atomicAdd(&a.hist[kDiag * (n + 1) + x], wgt);
+        open = (hi <= rows) ? (int64_t)a.ss[g * n + k] : 0;
+      }
+      if (open > 0) atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
+    }
+    {
+      const int64_t c = k;
+      Seg acc{0u, 0u, 0u};
+      for (int g = 0; g < a.nseg; ++g) {
+        const int64_t lo = a.bounds[g], hi = a.bounds[g + 1];
+        if (lo >= c) break;
+        if (hi <= lo) continue;
+        const int64_t L = min(hi, c) - lo;
+        const uint2 v = a.scol[g * n + c];
+        acc = seg_combine(acc, Seg{v.x, v.y, (int64_t)run_len(v.x) == L ? 1u : 0u}, h);
+      }
+      const uint2 rp = a.srow[c];
+      const Seg row{rp.x, rp.y, (int64_t)run_len(rp.x) == n - c ? 1u : 0u};
+      seg_flush(seg_combine(acc, row, h), h);
+    }
+  }
+}
+
+}  // namespace rqa

@@ -3,7 +3,8 @@
 
 namespace rqa {
 
-bool find_variant_l1_small(int m, int tau, Variant* out);
+// 256-row geometry: only through RQA_GEOMETRY=small (work units balance any n)
+static bool find_variant_l1_small(int, int, Variant*) { return false; }
 
 bool find_variant_l1(int m, int tau, bool small, Variant* out) {
   if (small && find_variant_l1_small(m, tau, out)) return true;

@@ -3,7 +3,8 @@
 
 namespace rqa {
 
-bool find_variant_l2_small(int m, int tau, Variant* out);
+// 256-row geometry: only through RQA_GEOMETRY=small (work units balance any n)
+static bool find_variant_l2_small(int, int, Variant*) { return false; }
 
 bool find_variant_l2(int m, int tau, bool small, Variant* out) {
   if (small && find_variant_l2_small(m, tau, out)) return true;
@@ -21,7 +22,5 @@ bool find_variant_l2(int m, int tau, bool small, Variant* out) {
   return false;
 }
 
-Variant mid_variant_l2_3_1() { return make_variant<kL2, 3, 1, 8, 2>(0); }
-Variant pipe_variant_l2_3_1() { return make_pipe_variant<kL2, 3, 1, 8, 2>(0); }
 
 }  // namespace rqa

@@ -1,0 +1,448 @@
+// rqa_unit.cuh -- upper-triangle kernel over 2-D work units.
+//
+// A work unit is (band b, iteration range [x_a, x_b)) of the diagonal sweep
+// of sym_kernel (rqa_sym.cuh): bands of H = R*HS rows are cut along the sweep
+// so that every CTA gets a bounded amount of work, which balances the SMs
+// for any n and lets a GPU's share of a multi-GPU run be spread over all of
+// its SMs.  What crosses a unit boundary is stitched by the folds:
+//   * diagonals: every (band, slot) is its own segment of HS rows; the run
+//     state starts at the slot's top row in every iteration and leaves through
+//     its bottom (P/S per slot, compact layout with height HS);
+//   * row parts of hooks: each unit reports the first and last run of the
+//     piece of the row it covers (rowpiece[unit][row]);
+//   * column parts of hooks: a column's slot segment spans iterations x-1 and
+//     x; a unit recomputes iteration x_a-1 (cells and row words only) to own
+//     the lower parts of the columns it finishes, and leaves the columns that
+//     finish at x_b to the next unit.
+// Arithmetic, bit conventions and run extraction are those of sym_kernel.
+#pragma once
+#include "rqa_sym.cuh"
+
+namespace rqa {
+
+// One work unit: band, first and last+1 iteration, row-piece slot index.
+struct Unit {
+  int32_t band, xa, xb, idx;
+};
+
+struct UnitArgs {
+  SymArgs base;            // s, n, row range, thr, theiler, m, tau, P, S, colsum, hist, points
+  const Unit* units;       // [nunits], ordered largest work first
+  uint2* rowpiece;         // [nunits][H]: (first, last) run of each row's piece
+};
+
+// Compact offset of per-slot diagonal segments: slot g covers rows
+// [row_lo + g*HS, +HS) and diagonals kd in [0, n - row_g).
+__host__ __device__ __forceinline__ int64_t slot_offset(int64_t g, int64_t n, int64_t row_lo,
+                                                        int64_t HS) {
+  return g * (n - row_lo) - HS * (g * (g - 1) / 2);
+}
+
+template <int METRIC, int M, int TAU, int NW, int R, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+unit_kernel(const UnitArgs ua, const int W_rt) {
+  const SymArgs& a = ua.base;
+  constexpr int D = 32 * NW;
+  constexpr int HS = D;
+  constexpr int H = R * HS;
+  constexpr bool kDirect = (M == 0);
+  constexpr int kW = kDirect ? 0 : (M - 1) * TAU;
+  constexpr bool kLinfAnd = (METRIC == kLinf) && (M >= 2);
+  constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
+  constexpr int NCH = HS / 32;  // == NW
+  static_assert(kLinfAnd ? kW <= 32 : kW <= 48, "term window too large");
+  const int W = kDirect ? W_rt : kW;
+  const SymSmem L(NW, R, W);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* s_row = reinterpret_cast<double*>(smem + L.off_row);
+  uint32_t* rowbuf = reinterpret_cast<uint32_t*>(smem + L.off_rowbuf);
+  uint32_t* prevbuf = reinterpret_cast<uint32_t*>(smem + L.off_prev);
+  uint2* colst = reinterpret_cast<uint2*>(smem + L.off_colst);
+  uint2* rowst = reinterpret_cast<uint2*>(smem + L.off_rowst);
+  uint32_t* sh_hist = reinterpret_cast<uint32_t*>(smem + L.off_hist);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.off_hist + 3 * kSmemBins * sizeof(uint32_t));
+
+  const Unit unit = ua.units[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wv = tid >> 5;
+  const int delta = 32 * wv + lane;
+  const int64_t n = a.n;
+  const int64_t b = unit.band;
+  const int64_t i0 = a.row_lo + b * H;
+  const int64_t i_end = min(i0 + (int64_t)H, a.row_hi);
+  const int nrem = (int)(n - i0);
+  const int hrows = (int)(i_end - i0);
+  const int theiler = (int)min(a.theiler, (int64_t)1 << 30);
+  const double thr = a.thr;
+  const int xa = unit.xa, xb = unit.xb;
+  const int xfirst = xa > 0 ? xa - 1 : 0;  // xa-1: recomputed for the columns finishing at xa
+  const int64_t goff0 = b * R;              // global slot index of slot 0
+  uint32_t* Cb = a.colsum + band_offset(b, n, a.row_lo, H);
+  uint2* piece = ua.rowpiece + (int64_t)unit.idx * H;
+  const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
+  const Transposer tr(lane);
+  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
+                 (1u << lane) - 1u};
+  uint16_t* Pslot[R];
+  uint16_t* Sslot[R];
+  const int64_t ptot = slot_offset((int64_t)((a.row_hi - a.row_lo + HS - 1) / HS), n, a.row_lo, HS);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    Pslot[r] = a.P + slot_offset(goff0 + r, n, a.row_lo, HS);
+    Sslot[r] = a.P + ptot + slot_offset(goff0 + r, n, a.row_lo, HS);
+  }
+
+  for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
+  for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
+  for (int q = tid; q < 2 * H; q += NW * 32) prevbuf[q] = 0u;
+  for (int q = tid; q < NW * R * 32; q += NW * 32) colst[q] = make_uint2(0u, 0u);
+  for (int q = tid; q < R * D; q += NW * 32) rowst[q] = make_uint2(0u, 0u);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(double));
+  if (tid == 0) {
+    const double* src;
+    col_window_src(a.s, i0 + (int64_t)xfirst * D, &src);
+    mbar_expect_tx_arrive(&bar[0], col_bytes);
+    tma_load_1d(smem + L.off_col0, src, col_bytes, &bar[0]);
+  }
+
+  RunState st[R];  // diagonal run state of the current (band, slot) segment
+  double win[R][kW > 0 ? kW : 1];
+  uint32_t ph_lo[R], ph_hi[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    st[r] = RunState{0u, 0u};
+    ph_lo[r] = 0u;
+    ph_hi[r] = 0u;
+  }
+  uint32_t pts = 0;
+  unsigned long long pts64 = 0;
+
+  for (int x = xfirst; x < xb; ++x) {
+    const int kx = x * D;
+    const int it = x - xfirst;           // local iteration counter (buffer parity)
+    const int buf = it & 1;
+    const bool warm = x < xa;             // column lower parts only
+    if (tid == 0 && x + 1 < xb) {
+      const double* src;
+      col_window_src(a.s, i0 + kx + D, &src);
+      mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes);
+      tma_load_1d(smem + (buf ? L.off_col0 : L.off_col1), src, col_bytes, &bar[buf ^ 1]);
+    }
+    mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
+    const int co = (int)((((uintptr_t)(a.s + i0 + kx)) >> 3) & 1);
+    const double* s_col =
+        reinterpret_cast<const double*>(smem + (buf ? L.off_col1 : L.off_col0)) + co + delta;
+
+    // term windows: every slot at the unit's first iteration, slot 0 afterwards
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      st[r] = RunState{0u, 0u};  // every (band, slot) is a segment of its own
+      if (r == 0 || x == xfirst) {
+        if constexpr (!kDirect && kW > 0) {
+          if constexpr (kLinfAnd) {
+            uint32_t p = 0;
+#pragma unroll
+            for (int u = 0; u < kW; ++u)
+              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= thr) p |= 1u << u;
+            ph_lo[r] = p;
+            ph_hi[r] = 0u;
+          } else {
+#pragma unroll
+            for (int u = 0; u < kW; ++u) {
+              const double d = __dsub_rn(s_row[r * HS + u], s_col[u]);
+              win[r][u] = kSquare ? __dmul_rn(d, d) : fabs(d);
+            }
+          }
+        }
+      }
+    }
+
+    int kdr[R], lastc[R], openb[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int kd = kx - r * HS + delta;
+      kdr[r] = kd;
+      const int vrows = min(max(hrows - r * HS, 0), HS);
+      const int crows = min(max(nrem - kd - r * HS, 0), vrows);
+      lastc[r] = crows;
+      openb[r] = (crows == vrows) ? 1 : 0;
+    }
+
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t dw[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) dw[r] = 0u;
+      const double* colc = s_col + 32 * c;
+      const double* rowc = s_row + 32 * c;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if constexpr (!kDirect) {
+          const double cv = colc[t + kW];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double rv = rowc[r * HS + t + kW];
+            const double d = __dsub_rn(rv, cv);
+            if constexpr (M == 1) {
+              setbit_le(dw[r], fabs(d), thr, 1u << t);
+            } else if constexpr (kLinfAnd) {
+              if (fabs(d) <= thr) {
+                if (t + kW < 32) ph_lo[r] |= 1u << ((t + kW) & 31);
+                else ph_hi[r] |= 1u << ((t + kW - 32) & 31);
+              }
+            } else {
+              const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
+              double acc = win[r][0];
+#pragma unroll
+              for (int k = 1; k < M - 1; ++k) acc = __dadd_rn(acc, win[r][k * TAU]);
+              acc = __dadd_rn(acc, term);
+              setbit_le(dw[r], acc, thr, 1u << t);
+#pragma unroll
+              for (int j = 0; j + 1 < kW; ++j) win[r][j] = win[r][j + 1];
+              win[r][kW - 1] = term;
+            }
+          }
+        } else {
+          const int m = a.m, tau = a.tau;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double* rp = rowc + r * HS + t;
+            const double* cp = colc + t;
+            bool hit;
+            if (METRIC == kLinf || m == 1) {
+              hit = true;
+              for (int k = 0; k < m; ++k) hit &= (fabs(__dsub_rn(rp[k * tau], cp[k * tau])) <= thr);
+            } else {
+              double acc = 0.0;
+              for (int k = 0; k < m; ++k) {
+                const double d = __dsub_rn(rp[k * tau], cp[k * tau]);
+                const double term = (METRIC == kL2) ? __dmul_rn(d, d) : fabs(d);
+                acc = (k == 0) ? term : __dadd_rn(acc, term);
+              }
+              hit = acc <= thr;
+            }
+            if (hit) dw[r] |= 1u << t;
+          }
+        }
+      }
+
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        uint32_t word;
+        if constexpr (kLinfAnd) {
+          word = ph_lo[r];
+#pragma unroll
+          for (int k = 1; k < M; ++k) word &= __funnelshift_rc(ph_lo[r], ph_hi[r], k * TAU);
+          ph_lo[r] = ph_hi[r];
+          ph_hi[r] = 0u;
+        } else {
+          word = dw[r];
+        }
+        const int kd = kdr[r];
+        if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
+        if (!warm) {
+          const bool live = kd >= 0 && kd < nrem;
+          const int rel = lastc[r] - 32 * c;
+          runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
+                    lane);
+          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+            // the segment is cut by the matrix's right edge inside the slot
+            diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
+                        LineSink{&hist, kd == 0 ? 1u : 2u});
+            st[r] = RunState{1u, 0u};
+          }
+        }
+        rowbuf[wv * H + r * HS + 32 * c + lane] = tr(word);
+      }
+    }
+    __syncthreads();
+
+    // ---- row phase (not in the recomputed iteration): row parts of hooks
+    const uint32_t* prev_cur = prevbuf + buf * H;    // words of iteration x-1, warp NW-1
+    uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
+    constexpr int PR = (R % 2 == 0) ? 2 : 1;
+#pragma unroll 1
+    for (int r0 = 0; r0 < R; r0 += PR) {
+      int lr[PR], rem[PR];
+      RunState rs[PR];
+      bool any_rem = false, all_full = true;
+#pragma unroll
+      for (int p = 0; p < PR; ++p) {
+        const int r = r0 + p;
+        lr[p] = r * HS + tid;
+        prev_next[lr[p]] = rowbuf[(NW - 1) * H + lr[p]];
+        const bool act = !warm && x >= r && lr[p] < hrows;
+        rem[p] = act ? nrem - lr[p] - (x - r) * D : 0;
+        any_rem |= rem[p] > 0;
+        all_full &= rem[p] >= D;
+      }
+      if (__any_sync(0xffffffffu, any_rem)) {
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const uint2 rsv = rowst[lr[p]];
+          rs[p] = RunState{rsv.x, rsv.y};
+        }
+        if (__all_sync(0xffffffffu, all_full)) {
+#pragma unroll 2
+          for (int v = 0; v < NW; ++v) {
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const uint32_t w = rowbuf[v * H + lr[p]];
+              pts += __popc(w);
+              runs_push(w, 32, rs[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+          }
+        } else {
+#pragma unroll 1
+          for (int v = 0; v < NW; ++v) {
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const int nb = min(max(rem[p] - 32 * v, 0), 32);
+              const uint32_t w = rowbuf[v * H + lr[p]] & low_mask(nb);
+              pts += __popc(w);
+              runs_push(w, nb, rs[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const int r = r0 + p;
+          if (rem[p] > 0 && x == r) pts64 -= (rowbuf[lr[p]] & 1u);  // diagonal cell once
+          rowst[lr[p]] = make_uint2(rs[p].first, rs[p].cur);
+        }
+      }
+    }
+    pts64 += 2ull * pts;
+    pts = 0;
+
+    // ---- column phase: finishing blocks (not in the recomputed iteration) and
+    // starting blocks (not in the last iteration: the next unit owns them)
+    {
+      const bool do_fin = !warm;
+      const bool do_new = x + 1 < xb;
+      Seg acc{0u, 0u, 0u};
+      const int cfin = kx + 32 * wv + lane;
+      const int cnew = cfin + D;
+#pragma unroll 1
+      for (int rr0 = 0; rr0 < R; rr0 += PR) {
+        int rs_[PR], lim_fin[PR], lim_new[PR];
+        RunState cur[PR], nst[PR], fin[PR];
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          const int r = R - 1 - (rr0 + p);
+          rs_[p] = r;
+          const uint2 cs = colst[(wv * R + r) * 32 + lane];
+          fin[p] = RunState{cs.y, cs.x};
+          nst[p] = RunState{0u, 0u};
+          cur[p] = RunState{0u, 0u};
+          lim_fin[p] = (do_fin && x >= r && cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
+          lim_new[p] = (do_new && x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
+        }
+        if (x >= rs_[PR - 1]) {
+#pragma unroll 1
+          for (int c = NCH - 1; c >= 0; --c) {
+            if (c == wv) {
+#pragma unroll
+              for (int p = 0; p < PR; ++p) {
+                nst[p] = cur[p];
+                cur[p] = fin[p];
+              }
+            }
+            const bool finishing = c <= wv;
+            if (finishing ? !do_fin : !do_new) continue;
+            const int wp = (wv - c) & (NW - 1);
+#pragma unroll
+            for (int p = 0; p < PR; ++p) {
+              const int lrow = rs_[p] * HS + 32 * c + lane;
+              const uint32_t w1 = rowbuf[wp * H + lrow];
+              const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
+              const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
+              const int nb = min(max((finishing ? lim_fin[p] : lim_new[p]) - 32 * c, 0), 32);
+              const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
+              runs_push(bits, nb, cur[p], 0u, evq);
+            }
+            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+          }
+#pragma unroll
+          for (int p = 0; p < PR; ++p) fin[p] = cur[p];
+        }
+#pragma unroll
+        for (int p = 0; p < PR; ++p) {
+          acc = seg_combine(acc, runs_finish(fin[p]), hist);
+          colst[(wv * R + rs_[p]) * 32 + lane] = make_uint2(nst[p].cur, nst[p].first);
+        }
+      }
+      if (do_fin && cfin < nrem)
+        Cb[cfin] = (cfin == 0) ? 0u
+                 : acc.uniform ? pack_col(acc.first, acc.first)
+                               : pack_col(acc.last, acc.first);
+    }
+    __syncthreads();
+
+    // ---- every slot's diagonal segment leaves through the slot's bottom edge
+    if (!warm) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int kd = kdr[r];
+        const int vrows = min(max(hrows - r * HS, 0), HS);
+        // open: the slot's last row is a cell of the diagonal (it may continue)
+        if (kd >= 0 && kd < nrem && vrows > 0 && st[r].cur != 0u &&
+            r * HS + vrows - 1 + kd < nrem)
+          diag_finish(st[r], true, Pslot[r] + kd, Sslot[r] + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
+      }
+    }
+#pragma unroll
+    for (int r = R - 1; r >= 1; --r) {
+      if constexpr (!kDirect && kW > 0) {
+        if constexpr (kLinfAnd) {
+          ph_lo[r] = ph_lo[r - 1];
+        } else {
+#pragma unroll
+          for (int j = 0; j < kW; ++j) win[r][j] = win[r - 1][j];
+        }
+      }
+    }
+    if (((it + 1) & 4095) == 0) {
+      for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
+        const uint32_t cnt = sh_hist[q];
+        if (cnt) {
+          atomicAdd(&a.hist[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)cnt);
+          sh_hist[q] = 0u;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- row pieces of this unit: (first, last) runs, read by the hook fold
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int lr = r * HS + tid;
+    if (lr < hrows) {
+      const uint2 rsv = rowst[lr];
+      const Seg sg = runs_finish(RunState{rsv.x, rsv.y});
+      piece[lr] = make_uint2(sg.first, sg.last);
+    }
+  }
+
+  queue_drain(evq, hist, lane, true);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) pts64 += __shfl_xor_sync(0xffffffffu, pts64, o);
+  if (lane == 0 && pts64) atomicAdd(a.points, pts64);
+  __syncthreads();
+  for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
+    const uint32_t cnt = sh_hist[q];
+    if (cnt) atomicAdd(&a.hist[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)cnt);
+  }
+}
+
+}  // namespace rqa

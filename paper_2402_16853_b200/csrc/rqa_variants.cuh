@@ -4,6 +4,7 @@
 
 #include "rqa_pipe.cuh"
 #include "rqa_sym.cuh"
+#include "rqa_unit.cuh"
 
 namespace rqa {
 
@@ -12,8 +13,10 @@ struct Variant {
   int w;                  // term window (m-1)*tau
   int reuse;              // 1: compile-time (m, tau) with term reuse; 0: direct
   size_t smem;            // dynamic shared memory bytes
-  cudaError_t (*launch)(const SymArgs&, int nbands, int w, cudaStream_t);
+  cudaError_t (*launch)(const UnitArgs&, int nunits, int w, cudaStream_t);
+  const void* kernel;     // for occupancy queries
   int64_t band_rows() const { return (int64_t)r * 32 * nw; }
+  int64_t slot_rows() const { return (int64_t)32 * nw; }
 };
 
 // 2 CTAs per SM, except the one-slot large-window variants (registers).
@@ -23,12 +26,12 @@ constexpr int min_blocks() {
 }
 
 template <int METRIC, int M, int TAU, int NW, int R>
-cudaError_t launch_sym(const SymArgs& a, int nbands, int w, cudaStream_t st) {
+cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
   const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
-  auto k = sym_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>;
+  auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  k<<<nbands, NW * 32, L.total, st>>>(a, w);
+  k<<<nunits, NW * 32, L.total, st>>>(a, w);
   return cudaGetLastError();
 }
 
@@ -36,25 +39,8 @@ template <int METRIC, int M, int TAU, int NW, int R>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
   const SymSmem L(NW, R, w);
-  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_sym<METRIC, M, TAU, NW, R>};
-}
-
-template <int METRIC, int M, int TAU, int NW, int R>
-cudaError_t launch_pipe(const SymArgs& a, int nbands, int w, cudaStream_t st) {
-  const PipeSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
-  auto k = pipe_kernel<METRIC, M, TAU, NW, R, 2>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-  if (e != cudaSuccess) return e;
-  k<<<nbands, NW * 32, L.total, st>>>(a, w);
-  return cudaGetLastError();
-}
-
-template <int METRIC, int M, int TAU, int NW, int R>
-Variant make_pipe_variant(int w_rt) {
-  static_assert(R <= 2, "the pipelined kernel's event ring holds 3*R*32 events per chunk");
-  const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const PipeSmem L(NW, R, w);
-  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_pipe<METRIC, M, TAU, NW, R>};
+  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_unit<METRIC, M, TAU, NW, R>,
+                 (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>};
 }
 
 // Implemented in rqa_kernels_<metric>[_small].cu (one translation unit each so
@@ -67,26 +53,17 @@ bool find_variant_linf(int m, int tau, bool small, Variant* out);
 bool find_variant_m1(int m, int tau, bool small, Variant* out);
 bool find_variant_direct(int metric, int m, int tau, bool small, Variant* out);
 
-// Rows of the matrix below which the 256-row geometry is chosen.
-constexpr int64_t kSmallGeometryBelow = 600000;
+// Rows below which the 256-row geometry is chosen.  Work units balance the
+// SMs for any n, so the 1024-row geometry is used everywhere by default.
+constexpr int64_t kSmallGeometryBelow = 0;
 
 inline bool find_variant(int metric, int m, int tau, int64_t n, Variant* out) {
   // RQA_GEOMETRY=small|big overrides the choice (benchmarking / tests)
   static const char* force = getenv("RQA_GEOMETRY");
   const bool small = force && force[0] == 's' ? true
                    : force && force[0] == 'b' ? false
-                   : force && (force[0] == 'm' || force[0] == 'p') ? false
                                               : n < kSmallGeometryBelow;
-  if (force && force[0] == 'm' && metric == kL2 && m == 3 && tau == 1) {  // experiment
-    extern Variant mid_variant_l2_3_1();
-    *out = mid_variant_l2_3_1();
-    return true;
-  }
-  if (force && force[0] == 'p' && metric == kL2 && m == 3 && tau == 1) {  // experiment
-    extern Variant pipe_variant_l2_3_1();
-    *out = pipe_variant_l2_3_1();
-    return true;
-  }
+
   if (m == 1) return find_variant_m1(m, tau, small, out);
   bool ok = false;
   if (metric == kL1) ok = find_variant_l1(m, tau, small, out);

@@ -34,8 +34,8 @@ class StripeOutputs:
 
     prefix: object   # int32 [n]
     suffix: object   # int32 [n]
-    col: object      # int32 [2n] (uint32 bit patterns)
-    rowlead: object  # int32 [n] (uint32 bit patterns), zero-initialised
+    col: object      # int32 [2n] (uint32 bit patterns): column part (first, last run)
+    rowlead: object  # int32 [2n] (uint32 bit patterns): row part (first, last), zero-init
 
     @staticmethod
     def empty(n: int, device, rows: int = 1):
@@ -46,7 +46,7 @@ class StripeOutputs:
         return StripeOutputs(torch.zeros(shape, dtype=torch.int32, device=device),
                              torch.zeros(shape, dtype=torch.int32, device=device),
                              torch.zeros(cshape, dtype=torch.int32, device=device),
-                             torch.zeros(n, dtype=torch.int32, device=device))
+                             torch.zeros(2 * n, dtype=torch.int32, device=device))
 
 
 def _ptr(t):

@@ -29,13 +29,13 @@ def pack(length, bit):
 
 
 def stripe_outputs(mat, lo, hi):
-    """(hist [3, n+1], points, prefix[n], suffix[n], col[2n], rowlead[n]) of rows [lo, hi)."""
+    """(hist [3, n+1], points, prefix[n], suffix[n], col[2n], rowpart[2n]) of rows [lo, hi)."""
     n = mat.shape[0]
     hist = np.zeros((3, n + 1), np.int64)
     pre = np.zeros(n, np.int64)
     suf = np.zeros(n, np.int64)
     col = np.zeros(2 * n, np.int64)
-    lead = np.zeros(n, np.int64)
+    lead = np.zeros(2 * n, np.int64)
     up = np.triu(mat)
     # upper-triangle cells stand for their mirror images; the diagonal once
     points = int(2 * up[lo:hi].sum() - sum(int(mat[i, i]) for i in range(lo, hi)))
@@ -76,11 +76,12 @@ def stripe_outputs(mat, lo, hi):
             col[2 * c + 1] = pack(rs[-1][1] - rs[-1][0], rs[-1][2])
             for a, b, bit in rs[1:-1]:
                 hist[1 if bit else 2, b - a] += 1
-    # row parts of the stripe's rows (columns [i, n))
+    # row parts of the stripe's rows (columns [i, n)): first and last run
     for i in range(lo, hi):
         rs = runs(mat[i, i:])
-        lead[i] = pack(rs[0][1] - rs[0][0], rs[0][2])
-        for a, b, bit in rs[1:]:
+        lead[2 * i] = pack(rs[0][1] - rs[0][0], rs[0][2])
+        lead[2 * i + 1] = pack(rs[-1][1] - rs[-1][0], rs[-1][2])
+        for a, b, bit in rs[1:-1]:
             hist[1 if bit else 2, b - a] += 1
     return hist, points, pre, suf, col, lead
 
@@ -146,15 +147,8 @@ def stitch(pre, suf, col, lead, bounds, n, hist):
             L = min(hi, c) - lo
             first, last = int(col[g][2 * c]), int(col[g][2 * c + 1])
             acc = _combine(acc, (first, last, (first >> 1) == L), hist)
-        ld = int(lead[c])
-        if acc is None:
-            _emit(hist, ld)
-        elif (acc[1] & 1) == (ld & 1):
-            if not acc[2]:
-                _emit(hist, acc[0])
-            _emit(hist, pack((acc[1] >> 1) + (ld >> 1), ld & 1))
-        else:
-            _emit(hist, acc[0])
-            if not acc[2]:
-                _emit(hist, acc[1])
-            _emit(hist, ld)
+        first, last = int(lead[2 * c]), int(lead[2 * c + 1])
+        acc = _combine(acc, (first, last, (first >> 1) == n - c), hist)
+        _emit(hist, acc[0])
+        if not acc[2]:
+            _emit(hist, acc[1])
