@@ -105,37 +105,62 @@ struct SymFoldArgs {
   uint2* out_col;
 };
 
+// Block-local line histogram of the fold kernels: shared 32-bit bins for
+// lengths < kSmemBins (runs that cross segment edges are plentiful, e.g. one
+// white run per hook and band), flushed once per block.
+struct FoldBins {
+  uint32_t* sh;
+  __device__ __forceinline__ void init() {
+    for (int q = threadIdx.x; q < 3 * kSmemBins; q += blockDim.x) sh[q] = 0u;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void flush(unsigned long long* g, int64_t n) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < 3 * kSmemBins; q += blockDim.x) {
+      const uint32_t c = sh[q];
+      if (c) atomicAdd(&g[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)c);
+    }
+  }
+};
+
 __host__ __device__ __forceinline__ int64_t sym_band_offset(int64_t b, int64_t n, int64_t row_lo,
                                                             int64_t H) {
   return b * (n - row_lo) - H * (b * (b - 1) / 2);
 }
 
-// Diagonal k >= 0 folded over the bands of [row_lo, row_hi); mode as fold_kernel.
+// Diagonal k >= 0 folded over the segments (height H) of [row_lo, row_hi);
+// mode as fold_kernel.  Offsets advance incrementally (compact layout).
 __global__ void sym_fold_diag(const SymFoldArgs a, const int mode) {
   const int64_t n = a.n;
+  __shared__ uint32_t bins[3 * kSmemBins];
+  FoldBins fb{bins};
+  fb.init();
+  const Hist h{smem_u32(bins), a.hist, n + 1};
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long wgt = (k == 0) ? 1ull : 2ull;
     const int64_t rows = n - k;
     int64_t open = 0, pstr = -1;
-    for (int g = 0; g < a.nb; ++g) {
-      const int64_t lo = a.row_lo + g * a.H;
+    int64_t lo = a.row_lo, off = k, stride = n - a.row_lo;
+    const int64_t nseg_k = min((int64_t)a.nb, (rows - a.row_lo + a.H - 1) / a.H);
+    for (int64_t g = 0; g < nseg_k; ++g) {
       const int64_t hi = min(lo + a.H, a.row_hi);
-      if (lo >= rows) break;
       const int64_t L = min(hi, rows) - lo;
-      const int64_t off = sym_band_offset(g, n, a.row_lo, a.H) + k;
       const int64_t p = (int64_t)a.P[off];
       if (p == L) {
         open += L;
-        continue;
+      } else {
+        const int64_t x = open + p;
+        if (mode == kFoldStripe && pstr < 0) pstr = x;
+        else if (x > 0) h.add(kDiag, x, (uint32_t)wgt);
+        open = (hi <= rows) ? (int64_t)a.S[off] : 0;
       }
-      const int64_t x = open + p;
-      if (mode == kFoldStripe && pstr < 0) pstr = x;
-      else if (x > 0) atomicAdd(&a.hist[kDiag * (n + 1) + x], wgt);
-      open = (hi <= rows) ? (int64_t)a.S[off] : 0;
+      lo += a.H;
+      off += stride;
+      stride -= a.H;
     }
     if (mode == kFoldFinal) {
-      if (open > 0) atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
+      if (open > 0) h.add(kDiag, open, (uint32_t)wgt);
     } else {
       int64_t sstr = 0;
       if (a.row_lo >= rows) {
@@ -146,12 +171,13 @@ __global__ void sym_fold_diag(const SymFoldArgs a, const int mode) {
       } else if (a.row_hi <= rows) {
         sstr = open;
       } else if (open > 0) {
-        atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
+        h.add(kDiag, open, (uint32_t)wgt);
       }
       a.out_p[k] = (int32_t)pstr;
       a.out_s[k] = (int32_t)sstr;
     }
   }
+  fb.flush(a.hist, n);
 }
 
 __device__ __forceinline__ void hook_finish(Seg acc, uint32_t lead, const GHist& h) {
@@ -265,19 +291,30 @@ struct UnitFoldArgs {
 
 __global__ void unit_fold_hooks(const UnitFoldArgs a, const int mode) {
   const int64_t n = a.n;
-  const GHist h{a.hist, n + 1};
+  __shared__ uint32_t bins[3 * kSmemBins];
+  FoldBins fb{bins};
+  fb.init();
+  const Hist h{smem_u32(bins), a.hist, n + 1};
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
     // column part: bands above row c
     Seg acc{0u, 0u, 0u};
-    for (int g = 0; g < a.nb; ++g) {
-      const int64_t lo = a.row_lo + g * a.H;
-      if (lo >= c) break;
-      const int64_t hi = min(lo + a.H, a.row_hi);
-      const int64_t L = min(hi, c) - lo;
-      const uint32_t v = a.colsum[sym_band_offset(g, n, a.row_lo, a.H) + (c - lo)];
-      const uint32_t top = v >> 16, bot = v & 0xffffu;
-      acc = seg_combine(acc, Seg{top, bot, (int64_t)run_len(top) == L ? 1u : 0u}, h);
+    {
+      int64_t lo = a.row_lo, off = c - a.row_lo, stride = n - a.row_lo;
+      for (int g = 0; g < a.nb && lo < c; ++g) {
+        const int64_t hi = min(lo + a.H, a.row_hi);
+        const int64_t L = min(hi, c) - lo;
+        const uint32_t v = a.colsum[off];
+        const uint32_t top = v >> 16, bot = v & 0xffffu;
+        if ((int64_t)run_len(top) == L && acc.uniform && run_bit(top) == run_bit(acc.first)) {
+          acc.first = acc.last = acc.first + (uint32_t)(L << 1);  // uniform + uniform, same bit
+        } else {
+          acc = seg_combine(acc, Seg{top, bot, (int64_t)run_len(top) == L ? 1u : 0u}, h);
+        }
+        lo += a.H;
+        off += stride - a.H;   // next band: offset grows by (n - lo_g), index shrinks by H
+        stride -= a.H;
+      }
     }
     // row part: pieces of row c (only if the row belongs to these bands)
     Seg row{0u, 0u, 0u};
@@ -303,6 +340,7 @@ __global__ void unit_fold_hooks(const UnitFoldArgs a, const int mode) {
       if (c >= a.row_lo && c < a.row_hi) a.out_row[c] = make_uint2(row.first, row.last);
     }
   }
+  fb.flush(a.hist, n);
 }
 
 // Final fold over stripes (multi-GPU) for the work-unit layout.
