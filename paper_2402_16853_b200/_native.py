@@ -13,7 +13,8 @@ from .errors import DeviceError, InvalidArgument, SeriesTooShort
 
 __all__ = ["lib", "LIB_PATH", "call", "SYMBOLS", "TIMING_SLOTS"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librqa_b200.so")
+LIB_PATH = os.environ.get("RQA_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "librqa_b200.so")  # RQA_LIB_PATH: A/B testing
 TIMING_SLOTS = 8
 
 _c = ctypes

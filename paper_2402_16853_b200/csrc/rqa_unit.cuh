@@ -247,7 +247,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
         const int kd = kdr[r];
         if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-        if (!warm) {
+        if (!warm && !(a.skip & 1)) {
           const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
           runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
@@ -283,7 +283,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         any_rem |= rem[p] > 0;
         all_full &= rem[p] >= D;
       }
-      if (__any_sync(0xffffffffu, any_rem)) {
+      if (!(a.skip & 2) && __any_sync(0xffffffffu, any_rem)) {
 #pragma unroll
         for (int p = 0; p < PR; ++p) {
           const uint2 rsv = rowst[lr[p]];
@@ -347,7 +347,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           lim_fin[p] = (do_fin && x >= r && cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
           lim_new[p] = (do_new && x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
         }
-        if (x >= rs_[PR - 1]) {
+        if (!(a.skip & 4) && x >= rs_[PR - 1]) {
 #pragma unroll 1
           for (int c = NCH - 1; c >= 0; --c) {
             if (c == wv) {
