@@ -114,6 +114,19 @@ int rqa_stitch_device(const int32_t *d_prefix, const int32_t *d_suffix, const ui
                       const uint32_t *d_rowpart, const int64_t *bounds, int32_t nstripes,
                       int64_t n, int64_t *d_hist, void *stream, char *err, size_t errlen);
 
+/*
+ * Recurrence-matrix block / recurrence plot (reference recurrence_block,
+ * embedding.py:115-171, and compute_plot/_or_reduce, plotting.py:48-109):
+ * rows [row0, row1) x columns [col0, col1) of the n x n matrix, OR-reduced in
+ * factor x factor blocks aligned to row0/col0, written row by row (row0 first)
+ * packed MSB-first and padded to whole bytes: ceil((row1-row0)/factor) rows of
+ * ceil(ceil((col1-col0)/factor)/8) bytes (numpy.packbits(axis=1) layout).
+ */
+int rqa_block(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+              double radius, int64_t theiler, int64_t row0, int64_t row1, int64_t col0,
+              int64_t col1, int32_t factor, int32_t device, uint8_t *out, char *err,
+              size_t errlen);
+
 /* FP64 pipe microbenchmark on `device`: sustained DADD and DMUL operations
  * per second (the roofline denominator of the FP64-bound band kernel). */
 int rqa_fp64_peak(int32_t device, double *dadd_per_s, double *dmul_per_s, char *err,

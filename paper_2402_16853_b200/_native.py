@@ -36,6 +36,8 @@ SYMBOLS = {
                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_char_p, _c.c_size_t]),
     "rqa_stitch_device": (_c.c_int, [_vp, _vp, _vp, _vp, _pi64, _i32, _i64, _vp, _vp,
                                      _c.c_char_p, _c.c_size_t]),
+    "rqa_block": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i64, _i64, _i64, _i64,
+                             _i32, _i32, _c.POINTER(_c.c_uint8), _c.c_char_p, _c.c_size_t]),
     "rqa_fp64_peak": (_c.c_int, [_i32, _pd, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_release": (_c.c_int, []),
 }

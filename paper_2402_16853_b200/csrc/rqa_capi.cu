@@ -406,6 +406,9 @@ __global__ void fp64_peak_kernel(double* out, int iters, double a) {
 }
 
 }  // namespace
+
+void note_launch() { g_launches++; }
+
 }  // namespace rqa
 
 using namespace rqa;
