@@ -85,7 +85,7 @@ def test_band_rows():
     assert lib.rqa_band_rows(1, 3, 1, 1 << 20, ctypes.byref(h), ctypes.byref(r)) == 0
     assert h.value == 1024 and r.value == 1
     assert lib.rqa_band_rows(1, 3, 1, 100000, ctypes.byref(h), ctypes.byref(r)) == 0
-    assert h.value == 256 and r.value == 1            # mid-size n: shorter bands
+    assert h.value == 1024 and r.value == 1           # work units balance any n
     assert lib.rqa_band_rows(0, 10, 5, 500000, ctypes.byref(h), ctypes.byref(r)) == 0
     assert r.value == 1                               # C4 has a reuse variant
     assert lib.rqa_band_rows(0, 17, 3, 500000, ctypes.byref(h), ctypes.byref(r)) == 0
