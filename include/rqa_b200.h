@@ -42,9 +42,12 @@ extern "C" {
 /* Number of timing slots written by rqa_run (seconds):
  * [0] h2d, [1] band kernel, [2] fold kernel, [3] d2h, [4] total device span,
  * [5] cells per second over the band+fold kernels, [6] band height,
- * [7] number of bands.  Very large n is split into row stripes processed
- * one after the other on the device when the band summaries would not fit. */
-#define RQA_TIMING_SLOTS 8
+ * [7] number of bands, [8] evaluation path (-1 float64 kernels, 0 f32 filter
+ * with float64 re-evaluation (exact), 1 fp32 mode), [9] certified band
+ * half-width of the f32 filter.  Very large n is split into row stripes
+ * processed one after the other on the device when the band summaries would
+ * not fit. */
+#define RQA_TIMING_SLOTS 10
 
 /* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
 int rqa_version(void);
@@ -75,6 +78,23 @@ int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t m
             int64_t *white, int64_t *points, double *timing, char *err, size_t errlen);
 
 /*
+ * rqa_run with a precision (the reference's run_analysis plus the
+ * `precision=` keyword of SURVEY.md 8b):
+ *   64: results bit-exact against the float64 reference.  Cells may be
+ *       evaluated in float32 inside a certified band test (the "f32
+ *       filter"); every word with a cell near the threshold is re-evaluated
+ *       in float64, so the histograms are identical either way.
+ *   32: fp32 mode -- samples, arithmetic and threshold in float32 (numpy
+ *       float32 semantics); *mismatches (may be NULL) receives the number of
+ *       cells of the full n x n matrix whose fp32 decision differs from the
+ *       float64 one.
+ */
+int rqa_run_prec(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                 double radius, int64_t theiler, int32_t precision, int32_t device,
+                 int64_t *diag, int64_t *vert, int64_t *white, int64_t *points,
+                 int64_t *mismatches, double *timing, char *err, size_t errlen);
+
+/*
  * Device-resident variant for callers that own device memory and a stream
  * (torch tensors): rows [row_lo, row_hi) of the recurrence matrix.
  *   mode 0 (final): rows must be [0, n); d_hist (int64[3*(n+1)], rows diag,
@@ -101,6 +121,15 @@ int rqa_run_device(const double *d_series, int64_t len, int32_t m, int32_t tau, 
                    int64_t *d_hist, int64_t *d_points, int32_t *d_stripe_prefix,
                    int32_t *d_stripe_suffix, uint32_t *d_stripe_col, uint32_t *d_rowpart,
                    void *stream, char *err, size_t errlen);
+
+/* rqa_run_device with a precision (64 or 32, see rqa_run_prec); in fp32 mode
+ * the mismatch count is ACCUMULATED into *d_mismatches (int64, device). */
+int rqa_run_device_prec(const double *d_series, int64_t len, int32_t m, int32_t tau,
+                        int32_t metric, double radius, int64_t theiler, int32_t precision,
+                        int64_t row_lo, int64_t row_hi, int32_t mode, int64_t *d_hist,
+                        int64_t *d_points, int64_t *d_mismatches, int32_t *d_stripe_prefix,
+                        int32_t *d_stripe_suffix, uint32_t *d_stripe_col, uint32_t *d_rowpart,
+                        void *stream, char *err, size_t errlen);
 
 /*
  * Cross-stripe stitch (engine.py:287-319 carry contract + flush :195-212):

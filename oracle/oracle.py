@@ -43,6 +43,16 @@ def _load():
             ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
             ctypes.c_int64, ctypes.c_int32, i64p, i64p, i64p, i64p]
         lib.oracle_run.restype = ctypes.c_int
+        lib.oracle_run_prec.argtypes = [
+            ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int32,
+            ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
+            ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, i64p, i64p, i64p, i64p, i64p]
+        lib.oracle_run_prec.restype = ctypes.c_int
+        lib.oracle_matrix_prec.argtypes = [
+            ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int32,
+            ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
+            ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8)]
+        lib.oracle_matrix_prec.restype = ctypes.c_int
         lib.oracle_matrix.argtypes = [
             ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int32,
             ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
@@ -84,15 +94,44 @@ def oracle_histograms(values, m, tau, metric, radius, theiler=0,
     return diag, vert, white, int(pts[0])
 
 
-def oracle_matrix(values, m, tau, metric, radius, theiler=0):
+def oracle_histograms_prec(values, m, tau, metric, radius, theiler=0,
+                           precision=64, tile_size=512, workers=None):
+    """As oracle_histograms, with precision 64 or 32 (fp32 mode extension);
+    returns (diag, vert, white, points, mismatched_cells), the last being the
+    number of cells of the full N x N matrix whose fp32 decision differs from
+    the float64 one (0 for precision 64)."""
+    lib = _load()
+    s = np.ascontiguousarray(values, dtype=np.float64)
+    n = s.shape[0] - (m - 1) * tau
+    if n < 1:
+        raise ValueError("series too short")
+    if workers is None:
+        workers = len(os.sched_getaffinity(0))
+    diag = np.zeros(n + 1, np.int64)
+    vert = np.zeros(n + 1, np.int64)
+    white = np.zeros(n + 1, np.int64)
+    pts = np.zeros(1, np.int64)
+    mism = np.zeros(1, np.int64)
+    rc = lib.oracle_run_prec(_ptr(s, ctypes.c_double), s.shape[0], m, tau,
+                             METRICS[metric], float(radius), int(theiler),
+                             int(tile_size), int(workers), int(precision),
+                             _ptr(diag, ctypes.c_int64), _ptr(vert, ctypes.c_int64),
+                             _ptr(white, ctypes.c_int64), _ptr(pts, ctypes.c_int64),
+                             _ptr(mism, ctypes.c_int64))
+    if rc != 0:
+        raise RuntimeError(f"oracle_run_prec failed with {rc}")
+    return diag, vert, white, int(pts[0]), int(mism[0])
+
+
+def oracle_matrix(values, m, tau, metric, radius, theiler=0, precision=64):
     """Full recurrence matrix (bool N x N) for small N."""
     lib = _load()
     s = np.ascontiguousarray(values, dtype=np.float64)
     n = s.shape[0] - (m - 1) * tau
     out = np.zeros((n, n), np.uint8)
-    rc = lib.oracle_matrix(_ptr(s, ctypes.c_double), s.shape[0], m, tau,
-                           METRICS[metric], float(radius), int(theiler),
-                           _ptr(out, ctypes.c_uint8))
+    rc = lib.oracle_matrix_prec(_ptr(s, ctypes.c_double), s.shape[0], m, tau,
+                                METRICS[metric], float(radius), int(theiler),
+                                int(precision), _ptr(out, ctypes.c_uint8))
     if rc != 0:
         raise RuntimeError(f"oracle_matrix failed with {rc}")
     return out.astype(bool)

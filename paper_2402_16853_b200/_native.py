@@ -15,7 +15,7 @@ __all__ = ["lib", "LIB_PATH", "call", "SYMBOLS", "TIMING_SLOTS"]
 
 LIB_PATH = os.environ.get("RQA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "librqa_b200.so")  # RQA_LIB_PATH: A/B testing
-TIMING_SLOTS = 8
+TIMING_SLOTS = 10
 
 _c = ctypes
 _i32, _i64, _dbl, _vp = _c.c_int32, _c.c_int64, _c.c_double, _c.c_void_p
@@ -32,6 +32,11 @@ SYMBOLS = {
     "rqa_band_rows": (_c.c_int, [_i32, _i32, _i32, _i64, _pi64, _pi32]),
     "rqa_run": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _pi64, _pi64,
                            _pi64, _pi64, _pd, _c.c_char_p, _c.c_size_t]),
+    "rqa_run_prec": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _i32, _pi64,
+                                _pi64, _pi64, _pi64, _pi64, _pd, _c.c_char_p, _c.c_size_t]),
+    "rqa_run_device_prec": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _i64,
+                                       _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       _c.c_char_p, _c.c_size_t]),
     "rqa_run_device": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _dbl, _i64, _i64, _i64, _i32,
                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_char_p, _c.c_size_t]),
     "rqa_stitch_device": (_c.c_int, [_vp, _vp, _vp, _vp, _pi64, _i32, _i64, _vp, _vp,

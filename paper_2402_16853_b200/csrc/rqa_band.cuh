@@ -76,11 +76,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-// Stage s[i0+k_x+q] (q in [0, CW-1)) into a column buffer; returns the 0/1
+// Stage s[i0+k_x+q] (q in [0, CW-1)) into a column buffer; returns the
 // element offset introduced by aligning the source down to 16 bytes.
-__device__ __forceinline__ int col_window_src(const double* s, int64_t start, const double** src) {
+template <typename T>
+__device__ __forceinline__ int col_window_src(const T* s, int64_t start, const T** src) {
   const uintptr_t a = (uintptr_t)(s + start);
-  const int off = (int)((a >> 3) & 1);
+  const int off = (int)((a & 15u) / sizeof(T));
   *src = s + start - off;
   return off;
 }

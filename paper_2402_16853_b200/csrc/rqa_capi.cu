@@ -47,11 +47,31 @@ double threshold_for(int metric, int m, double radius) {
   return (metric == kL2 && m > 1) ? l2_threshold(radius) : radius;
 }
 
+// fp32-mode threshold: T*32 = max{x : sqrtf(x) <= fl32(eps)} for L2 with
+// m > 1, else fl32(radius) (numpy float32 semantics, oracle/rqa_oracle.c).
+float threshold_for32(int metric, int m, double radius) {
+  const float eps = (float)radius;
+  if (!(metric == kL2 && m > 1)) return eps;
+  if (std::isinf(eps)) return INFINITY;
+  float t = eps * eps;
+  if (std::isinf(t)) t = FLT_MAX;
+  while (t > 0.0f && std::sqrt(t) > eps) t = std::nextafter(t, 0.0f);
+  for (;;) {
+    const float u = std::nextafter(t, INFINITY);
+    if (std::isinf(u) || std::sqrt(u) > eps) break;
+    t = u;
+  }
+  return t;
+}
+
 struct Workspace {
   std::mutex mu;
   cudaStream_t stream = nullptr;
   double* s_pad = nullptr;
   size_t s_cap = 0;  // elements
+  float* sf_pad = nullptr;     // f32 filter: samples rounded to float32
+  size_t sf_cap = 0;
+  unsigned long long* maxbits = nullptr;  // max |s| as float64 bits (NaN/inf: >= 0x7ff0...)
   uint16_t* ps = nullptr;      // P and S (compact band layout)
   size_t ps_cap = 0;  // elements
   uint32_t* cs = nullptr;      // column-part summaries (compact band layout)
@@ -69,7 +89,8 @@ struct Workspace {
   int32_t* stripe_buf = nullptr;  // auto-striping: [G][n] x2 + [G][2n] + [2n]
   size_t stripe_buf_cap = 0;
   unsigned long long* hist = nullptr;
-  size_t hist_cap = 0;  // elements (3*(n+1) + 1 for points)
+  size_t hist_cap = 0;  // elements (3*(n+1) + 2: points, fp32 mismatches)
+  size_t maxbits_cap = 0;
   int64_t* bounds = nullptr;
   size_t bounds_cap = 0;
   cudaEvent_t ev[6] = {};
@@ -104,6 +125,13 @@ struct Problem {
   int64_t theiler;
   Variant var;
   int64_t pad;  // zero padding on each side of the staged series
+  // precision (rqa_unit.cuh f32 filter)
+  int precision = 64;   // 64 or 32 (fp32 mode)
+  int filt = -1;        // -1: float64 kernel; 0: f32 filter, exact; 1: fp32 mode
+  float c32 = 0.f, band32 = 0.f, thr32 = 0.f;
+  int all_amb = 0;
+  const float* sf = nullptr;
+  unsigned long long* mism = nullptr;
 };
 
 int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
@@ -134,10 +162,68 @@ int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
     return set_err(err, errlen, "embedding window (m-1)*tau = %lld too large (max 4096)",
                    (long long)span),
            RQA_EINVAL;
-  const int64_t H = p->var.band_rows(), D = 32 * p->var.nw;
+  // padding for every geometry (f32 variants may use other band heights)
+  const int64_t H = std::max<int64_t>(p->var.band_rows(), 1024), D = 256;
   p->pad = 2 * H + 4 * D + p->var.w + 256;
-  (void)D;
   return RQA_OK;
+}
+
+// Certified band of the f32 filter.  With M = max|s| (finite data) every
+// float32 difference is bounded against its float64 counterpart (u = 2^-24,
+// v = 2^-53, eta = 2^-149 absolute for float32 subnormals):
+//   |d32 - d64| <= dd = 4.5 u M + 4 v M + 4 eta   (rounded inputs + subtraction)
+// The float64 decision is acc64 <= T64, the float32 one acc32 - c32 < 0.
+// Suppose |acc32 - c32| > B and the decisions differ.  Either acc32 < c32,
+// or acc64 <= T64; in both cases every (non-negative) term of that sum is at
+// most T'' = max(c32, T64) (1 + 4 m u), so |d| <= sqrt(T'') + dd for both
+// precisions, and
+//   L2:  |acc32 - acc64| <= E = m [dd (2 sqrt(T'') + dd) + (u + v) T''] + (m-1)(u + v) T'' 1.01
+//   L1:  E = m dd + (m-1)(u + v) T'' 1.01
+//   L-inf / m = 1 (per component): E = dd
+// (+ 3 m eta for float32 underflow).  With B >= E + |c32 - T64| the first
+// case gives acc64 < c32 - B + E <= T64 and the second acc32 <= T64 + E <
+// c32 + B: both contradict.  B carries a further safety factor 2.  Cells
+// whose float32 sum overflows are far outside the band and out in both
+// precisions (T64 <= 1e30).
+bool f32_band(const Problem& p, double maxabs, bool finite, float c32, float* band) {
+  const double u = std::ldexp(1.0, -24), v = std::ldexp(1.0, -53), eta = std::ldexp(1.0, -149);
+  const double M = maxabs, m = p.m;
+  if (!finite || !(M <= 1e15) || !std::isfinite(c32) || !(c32 >= 1e-30f) || !(c32 <= 1e30f) ||
+      !(p.thr <= 1e30))
+    return false;
+  const double dd = 4.5 * u * M + 4.0 * v * M + 4.0 * eta;
+  const double T2 = std::max((double)c32, p.thr) * (1.0 + 4.0 * m * u);
+  double E;
+  if (p.metric == kL2 && p.m > 1) {
+    E = m * (dd * (2.0 * std::sqrt(T2) + dd) + (u + v) * T2) + (m - 1.0) * (u + v) * T2 * 1.01;
+  } else if (p.metric == kL1 && p.m > 1) {
+    E = m * dd + (m - 1.0) * (u + v) * T2 * 1.01;
+  } else {
+    E = dd;
+  }
+  E += 3.0 * m * eta;
+  const double B = 2.0 * (E + std::fabs((double)c32 - p.thr)) + eta;
+  if (!(B < 1e30)) return false;
+  *band = std::nextafter((float)B, INFINITY);
+  return true;
+}
+
+__global__ void prep_f32_kernel(const double* __restrict__ s, float* __restrict__ sf, int64_t count,
+                                unsigned long long* maxbits) {
+  unsigned long long mx = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double x = s[q];
+    sf[q] = __double2float_rn(x);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+    mx = b > mx ? b : mx;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = y > mx ? y : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxbits, mx);
 }
 
 int cuda_fail(cudaError_t e, const char* what, char* err, size_t errlen) {
@@ -161,6 +247,58 @@ int stage_series(Workspace* ws, const Problem& p, const double* src, cudaMemcpyK
            "memset pad");
   RQA_CUDA(cudaMemcpyAsync(ws->s_pad + p.pad, src, (size_t)p.len * sizeof(double), kind, st),
            "copying series");
+  return RQA_OK;
+}
+
+// Precision plan after the series is staged: precision 32 always runs the f32
+// kernels (fp32 mode).  Precision 64 runs the float64 kernels by default: the
+// f32 filter issues 8 % fewer instructions on C3 but moves the evaluation
+// from the otherwise idle FP64 pipe onto the FMA/ALU pipes the run
+// bookkeeping saturates, and measured 3 % slower (profiles/r01_ncu_f32_vs_fp64.txt).
+// RQA_FILTER=1 enables it when the band is certifiable and narrow (band <=
+// 1e-2 of the threshold) and a packed variant exists; RQA_FILTER=2 drops the
+// width condition (tests).  Results are bit-identical on every path.
+int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
+  p->filt = -1;
+  static const char* fenv = getenv("RQA_FILTER");
+  const int want = fenv ? atoi(fenv) : 0;
+  Variant fv;
+  const bool packed = find_variant_f32(p->metric, p->m, p->tau, true, &fv);
+  if (p->precision == 64 && (want == 0 || !packed)) return RQA_OK;
+  const size_t count = (size_t)(p->len + 2 * p->pad);
+  RQA_CUDA(grow(&ws->sf_pad, &ws->sf_cap, count), "allocating float32 series");
+  RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 1), "allocating");
+  RQA_CUDA(cudaMemsetAsync(ws->maxbits, 0, sizeof(unsigned long long), st), "memset");
+  prep_f32_kernel<<<148 * 4, 256, 0, st>>>(ws->s_pad, ws->sf_pad, (int64_t)count, ws->maxbits);
+  RQA_CUDA(cudaGetLastError(), "launching f32 staging");
+  g_launches++;
+  unsigned long long mb = 0;
+  RQA_CUDA(cudaMemcpyAsync(&mb, ws->maxbits, sizeof mb, cudaMemcpyDeviceToHost, st), "d2h");
+  RQA_CUDA(cudaStreamSynchronize(st), "f32 staging");
+  const bool finite = mb < 0x7ff0000000000000ull;
+  double maxabs;
+  memcpy(&maxabs, &mb, sizeof maxabs);
+  p->sf = ws->sf_pad + p->pad;
+  if (p->precision == 32) {
+    const float t32 = threshold_for32(p->metric, p->m, p->radius);
+    p->thr32 = t32;
+    p->c32 = std::nextafter(t32, INFINITY);
+    p->all_amb = f32_band(*p, maxabs, finite, p->c32, &p->band32) ? 0 : 1;
+    p->filt = 1;
+    if (!find_variant_f32(p->metric, p->m, p->tau, false, &p->var))
+      return set_err(err, errlen, "no fp32 kernel for this embedding"), RQA_EINVAL;
+    return RQA_OK;
+  }
+  const float c = (float)p->thr;
+  float band = 0.f;
+  if (!f32_band(*p, maxabs, finite, c, &band)) return RQA_OK;
+  if (want != 2 && !(band <= 1e-2f * c)) return RQA_OK;
+  p->c32 = c;
+  p->thr32 = std::nextafter(c, -INFINITY);  // acc32 <= thr32  <=>  acc32 < c32
+  p->band32 = band;
+  p->all_amb = 0;
+  p->filt = 0;
+  p->var = fv;
   return RQA_OK;
 }
 
@@ -276,6 +414,13 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   static const char* skip_env = getenv("RQA_SKIP");  // profiling only: skip phases
   a.skip = skip_env ? atoi(skip_env) : 0;
   a.timers = nullptr;
+  a.sf = p.sf;
+  a.c32 = p.c32;
+  a.band32 = p.band32;
+  a.thr32 = p.thr32;
+  a.prec_mode = p.filt == 1 ? 1 : 0;
+  a.all_amb = p.all_amb;
+  a.mism = p.mism;
   ua.units = ws->units;
   ua.rowpiece = ws->rowpiece;
   RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
@@ -445,14 +590,18 @@ int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t* ba
   return RQA_OK;
 }
 
-int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
-            double radius, int64_t theiler, int32_t device, int64_t* diag, int64_t* vert,
-            int64_t* white, int64_t* points, double* timing, char* err, size_t errlen) {
+int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                 double radius, int64_t theiler, int32_t precision, int32_t device,
+                 int64_t* diag, int64_t* vert, int64_t* white, int64_t* points,
+                 int64_t* mismatches, double* timing, char* err, size_t errlen) {
   if (!series || !diag || !vert || !white || !points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
+  if (precision != 64 && precision != 32)
+    return set_err(err, errlen, "precision must be 64 or 32"), RQA_EINVAL;
   Problem p;
   int rc = validate(len, m, tau, metric, radius, theiler, &p, err, errlen);
   if (rc) return rc;
+  p.precision = precision;
   int ndev = rqa_device_count();
   if (ndev <= 0) return set_err(err, errlen, "no CUDA device available"), RQA_EDEVICE;
   if (device < 0 || device >= ndev)
@@ -467,11 +616,14 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
   }
   cudaStream_t st = ws->stream;
   const size_t hn = (size_t)(p.n + 1);
-  RQA_CUDA(grow(&ws->hist, &ws->hist_cap, 3 * hn + 1), "allocating histograms");
+  RQA_CUDA(grow(&ws->hist, &ws->hist_cap, 3 * hn + 2), "allocating histograms");
   RQA_CUDA(cudaEventRecord(ws->ev[0], st), "event");
   rc = stage_series(ws, p, series, cudaMemcpyHostToDevice, st, err, errlen);
   if (rc) return rc;
-  RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 1) * sizeof(unsigned long long), st), "memset");
+  RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 2) * sizeof(unsigned long long), st), "memset");
+  rc = plan_precision(ws, &p, st, err, errlen);
+  if (rc) return rc;
+  p.mism = ws->hist + 3 * hn + 1;
   RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
   rc = run_full(ws, p, ws->hist, ws->hist + 3 * hn, st, ws->ev[2], err, errlen);
   if (rc) return rc;
@@ -480,6 +632,9 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
   RQA_CUDA(cudaMemcpyAsync(vert, ws->hist + hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
   RQA_CUDA(cudaMemcpyAsync(white, ws->hist + 2 * hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
   RQA_CUDA(cudaMemcpyAsync(points, ws->hist + 3 * hn, 8, cudaMemcpyDeviceToHost, st), "d2h");
+  if (mismatches)
+    RQA_CUDA(cudaMemcpyAsync(mismatches, ws->hist + 3 * hn + 1, 8, cudaMemcpyDeviceToHost, st),
+             "d2h");
   RQA_CUDA(cudaEventRecord(ws->ev[4], st), "event");
   RQA_CUDA(cudaStreamSynchronize(st), "running kernels");
   if (timing) {
@@ -496,20 +651,35 @@ int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t m
     timing[5] = kern > 0 ? (double)p.n * (double)p.n / kern : 0.0;
     timing[6] = (double)p.var.band_rows();
     timing[7] = (double)((p.n + p.var.band_rows() - 1) / p.var.band_rows());
+    timing[8] = (double)p.filt;
+    timing[9] = (double)p.band32;
   }
   return RQA_OK;
 }
 
-int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
-                   double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
-                   int64_t* d_hist, int64_t* d_points, int32_t* d_stripe_prefix,
-                   int32_t* d_stripe_suffix, uint32_t* d_stripe_col, uint32_t* d_rowlead,
-                   void* stream, char* err, size_t errlen) {
+int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+            double radius, int64_t theiler, int32_t device, int64_t* diag, int64_t* vert,
+            int64_t* white, int64_t* points, double* timing, char* err, size_t errlen) {
+  return rqa_run_prec(series, len, m, tau, metric, radius, theiler, 64, device, diag, vert, white,
+                      points, nullptr, timing, err, errlen);
+}
+
+int rqa_run_device_prec(const double* d_series, int64_t len, int32_t m, int32_t tau,
+                        int32_t metric, double radius, int64_t theiler, int32_t precision,
+                        int64_t row_lo, int64_t row_hi, int32_t mode, int64_t* d_hist,
+                        int64_t* d_points, int64_t* d_mismatches, int32_t* d_stripe_prefix,
+                        int32_t* d_stripe_suffix, uint32_t* d_stripe_col, uint32_t* d_rowlead,
+                        void* stream, char* err, size_t errlen) {
   if (!d_series || !d_hist || !d_points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
+  if (precision != 64 && precision != 32)
+    return set_err(err, errlen, "precision must be 64 or 32"), RQA_EINVAL;
+  if (precision == 32 && !d_mismatches)
+    return set_err(err, errlen, "fp32 mode needs a mismatch counter"), RQA_EINVAL;
   Problem p;
   int rc = validate(len, m, tau, metric, radius, theiler, &p, err, errlen);
   if (rc) return rc;
+  p.precision = precision;
   if (mode != kFoldFinal && mode != kFoldStripe)
     return set_err(err, errlen, "mode must be 0 (final) or 1 (stripe)"), RQA_EINVAL;
   if (row_lo < 0 || row_hi > p.n || row_lo > row_hi)
@@ -528,14 +698,30 @@ int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, 
   cudaStream_t st = (cudaStream_t)stream;
   rc = stage_series(ws, p, d_series, cudaMemcpyDeviceToDevice, st, err, errlen);
   if (rc) return rc;
-  const size_t hn = (size_t)(p.n + 1);
-  (void)hn;
+  rc = plan_precision(ws, &p, st, err, errlen);
+  if (rc) return rc;
+  if (p.filt == 0 && !d_mismatches) {  // exact filter: counter unused but must exist
+    RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 1), "allocating");
+    p.mism = ws->maxbits;
+  } else {
+    p.mism = reinterpret_cast<unsigned long long*>(d_mismatches);
+  }
   if (mode == kFoldFinal)
     return run_full(ws, p, reinterpret_cast<unsigned long long*>(d_hist),
                     reinterpret_cast<unsigned long long*>(d_points), st, nullptr, err, errlen);
   return launch_rows(ws, p, row_lo, row_hi, mode, reinterpret_cast<unsigned long long*>(d_hist),
                      reinterpret_cast<unsigned long long*>(d_points), d_stripe_prefix,
                      d_stripe_suffix, d_stripe_col, d_rowlead, st, nullptr, err, errlen);
+}
+
+int rqa_run_device(const double* d_series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                   double radius, int64_t theiler, int64_t row_lo, int64_t row_hi, int32_t mode,
+                   int64_t* d_hist, int64_t* d_points, int32_t* d_stripe_prefix,
+                   int32_t* d_stripe_suffix, uint32_t* d_stripe_col, uint32_t* d_rowlead,
+                   void* stream, char* err, size_t errlen) {
+  return rqa_run_device_prec(d_series, len, m, tau, metric, radius, theiler, 64, row_lo, row_hi,
+                             mode, d_hist, d_points, nullptr, d_stripe_prefix, d_stripe_suffix,
+                             d_stripe_col, d_rowlead, stream, err, errlen);
 }
 
 int rqa_stitch_device(const int32_t* d_prefix, const int32_t* d_suffix, const uint32_t* d_col,
@@ -602,6 +788,8 @@ int rqa_release(void) {
     if (!ws) continue;
     cudaSetDevice((int)d);
     cudaFree(ws->s_pad);
+    cudaFree(ws->sf_pad);
+    cudaFree(ws->maxbits);
     cudaFree(ws->ps);
     cudaFree(ws->cs);
     cudaFree(ws->rowlead);

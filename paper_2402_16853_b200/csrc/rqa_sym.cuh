@@ -36,6 +36,16 @@ struct SymArgs {
   unsigned long long* points;
   int skip;                  // profiling only (RQA_SKIP): 1 diag runs, 2 row phase, 4 column phase
   unsigned long long* timers;  // profiling only (RQA_TIMERS): [4] cycles compute/rows/cols/other
+  // f32 filter kernels (PREC = 1, rqa_unit.cuh): float32 evaluation with a
+  // certified band around the threshold; words with a cell inside the band
+  // are re-evaluated in float64 (and, in fp32 mode, in scalar float32).
+  const float* sf;           // device samples rounded to float32, same padding as s
+  float c32;                 // band centre: fast-path bit = (acc32 - c32 < 0)
+  float band32;              // half-width: |acc32 - c32| <= band32 is ambiguous
+  float thr32;               // fp32-mode threshold (T*32 for L2 with m > 1, else fl32(radius))
+  int prec_mode;             // 0: exact (ambiguous words take the float64 bits); 1: fp32 mode
+  int all_amb;               // 1: every word is re-evaluated (band not certifiable)
+  unsigned long long* mism;  // fp32 mode: cells whose fp32 and fp64 decisions differ
 };
 
 // Compact per-band offset of entries kd (or c - i0) in [0, n - i0).
@@ -53,17 +63,26 @@ struct SymSmem {
   int H, HS, D, W, CW;
   size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_rowst, off_queue,
       off_hist, total;
-  __host__ __device__ SymSmem(int NW, int R, int W_) {
+  // esize 8: float64 row/column windows; 4: float32 windows (f32 filter
+  // kernels), the row window stored as R/2 interleaved slot pairs of
+  // HS + W + 4 float2 each (rqa_unit.cuh, packed f32x2 evaluation).
+  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8) {
     D = 32 * NW;
     HS = D;
     H = R * HS;
     W = W_;
-    CW = ((HS + D + W + 2) + 1) & ~1;
     off_row = 0;
-    const size_t row_elems = ((size_t)(H + W) + 2) & ~(size_t)1;
-    off_col0 = off_row + row_elems * sizeof(double);
-    off_col1 = off_col0 + (size_t)CW * sizeof(double);
-    off_rowbuf = off_col1 + (size_t)CW * sizeof(double);
+    if (esize == 8) {
+      CW = ((HS + D + W + 2) + 1) & ~1;
+      const size_t row_elems = ((size_t)(H + W) + 2) & ~(size_t)1;
+      off_col0 = off_row + row_elems * sizeof(double);
+    } else {
+      CW = ((HS + D + W + 4) + 3) & ~3;  // TMA sizes are multiples of 16 bytes
+      const size_t row_bytes = (size_t)(R + 1) * (HS + W + 4) * sizeof(float);
+      off_col0 = off_row + ((row_bytes + 15) & ~(size_t)15);
+    }
+    off_col1 = off_col0 + (size_t)CW * esize;
+    off_rowbuf = off_col1 + (size_t)CW * esize;
     off_prev = off_rowbuf + (size_t)NW * H * sizeof(uint32_t);
     off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
     off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);

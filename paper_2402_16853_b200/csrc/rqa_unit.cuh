@@ -16,6 +16,8 @@
 //     finish at x_b to the next unit.
 // Arithmetic, bit conventions and run extraction are those of sym_kernel.
 #pragma once
+#include <type_traits>
+
 #include "rqa_sym.cuh"
 
 namespace rqa {
@@ -38,7 +40,71 @@ __host__ __device__ __forceinline__ int64_t slot_offset(int64_t g, int64_t n, in
   return g * (n - row_lo) - HS * (g * (g - 1) / 2);
 }
 
-template <int METRIC, int M, int TAU, int NW, int R, int MINB>
+// ---------------------------------------------------------------------------
+// f32 filter (PREC = 1).  Cells are evaluated in float32 (packed f32x2 over
+// slot pairs for the L1/L2 term-reuse kernels); the bit of a cell is the sign
+// of acc32 - c32.  The host certifies a band |acc32 - c32| <= band32 outside
+// which the float32 decision equals the float64 one (rqa_capi.cu,
+// f32_band); a word with a cell inside the band is re-evaluated here, in
+// float64 with the reference's operation order (and in scalar float32 with
+// the fp32-mode semantics, for the mismatch count).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long x, unsigned long long y) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long x, unsigned long long y) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float f2_lo(unsigned long long x) { return __uint_as_float((uint32_t)x); }
+__device__ __forceinline__ float f2_hi(unsigned long long x) {
+  return __uint_as_float((uint32_t)(x >> 32));
+}
+
+// Re-evaluate the 32 cells (row0 + t, row0 + t + kd), t = 0..31, of one word:
+// x = float64 bits (reference semantics, threshold a.thr), y = float32 bits
+// (fp32-mode semantics: samples, ufuncs and threshold in float32).
+template <int METRIC>
+__device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int64_t kd) {
+  const int m = a.m, tau = a.tau;
+  const bool per_comp = (METRIC == kLinf) || m == 1;
+  uint32_t w64 = 0u, w32 = 0u;
+  for (int t = 0; t < 32; ++t) {
+    const int64_t i = row0 + t, j = i + kd;
+    bool h64 = true, h32 = true;
+    double acc = 0.0;
+    float acc32 = 0.0f;
+    for (int k = 0; k < m; ++k) {
+      const int64_t o = (int64_t)k * tau;
+      const double d = __dsub_rn(a.s[i + o], a.s[j + o]);
+      const float d32 = __fsub_rn(a.sf[i + o], a.sf[j + o]);
+      if (per_comp) {
+        h64 &= fabs(d) <= a.thr;
+        h32 &= fabsf(d32) <= a.thr32;
+      } else {
+        const double tm = (METRIC == kL2) ? __dmul_rn(d, d) : fabs(d);
+        const float tm32 = (METRIC == kL2) ? __fmul_rn(d32, d32) : fabsf(d32);
+        acc = (k == 0) ? tm : __dadd_rn(acc, tm);
+        acc32 = (k == 0) ? tm32 : __fadd_rn(acc32, tm32);
+      }
+    }
+    if (!per_comp) {
+      h64 = acc <= a.thr;
+      h32 = acc32 <= a.thr32;
+    }
+    w64 |= (h64 ? 1u : 0u) << t;
+    w32 |= (h32 ? 1u : 0u) << t;
+  }
+  return make_uint2(w64, w32);
+}
+
+template <int METRIC, int M, int TAU, int NW, int R, int MINB, int PREC = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
 unit_kernel(const UnitArgs ua, const int W_rt) {
   const SymArgs& a = ua.base;
@@ -51,11 +117,19 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
   constexpr int NCH = HS / 32;  // == NW
   static_assert(kLinfAnd ? kW <= 32 : kW <= 48, "term window too large");
+  constexpr bool kF32 = (PREC == 1);
+  // packed f32x2 evaluation over slot pairs (2r, 2r+1): L1/L2 term reuse
+  constexpr bool kPacked = kF32 && !kDirect && !kLinfAnd && M >= 2 && (R % 2 == 0);
+  static_assert(!kF32 || kDirect || kPacked, "f32 filter: packed reuse or direct kernels");
+  using F = typename std::conditional<kF32, float, double>::type;
+  constexpr int RP = (R + 1) / 2;  // slot pairs
   const int W = kDirect ? W_rt : kW;
-  const SymSmem L(NW, R, W);
+  const SymSmem L(NW, R, W, (int)sizeof(F));
+  const int PS = HS + W + 4;       // packed row window: float2 elements per slot pair
 
   extern __shared__ __align__(128) unsigned char smem[];
-  double* s_row = reinterpret_cast<double*>(smem + L.off_row);
+  F* s_row = reinterpret_cast<F*>(smem + L.off_row);
+  float2* s_row2 = reinterpret_cast<float2*>(smem + L.off_row);
   uint32_t* rowbuf = reinterpret_cast<uint32_t*>(smem + L.off_rowbuf);
   uint32_t* prevbuf = reinterpret_cast<uint32_t*>(smem + L.off_prev);
   uint2* colst = reinterpret_cast<uint2*>(smem + L.off_colst);
@@ -94,8 +168,17 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     Sslot[r] = a.P + ptot + slot_offset(goff0 + r, n, a.row_lo, HS);
   }
 
+  const F* gs;  // samples the windows are staged from
+  if constexpr (kF32) gs = a.sf; else gs = a.s;
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
-  for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];
+  if constexpr (kPacked) {
+    for (int q = tid; q < RP * (HS + W); q += NW * 32) {
+      const int pr = q / (HS + W), u = q - pr * (HS + W);
+      s_row2[pr * PS + u] = make_float2(gs[i0 + 2 * pr * HS + u], gs[i0 + (2 * pr + 1) * HS + u]);
+    }
+  } else {
+    for (int q = tid; q < H + W; q += NW * 32) s_row[q] = gs[i0 + q];
+  }
   for (int q = tid; q < 2 * H; q += NW * 32) prevbuf[q] = 0u;
   for (int q = tid; q < NW * R * 32; q += NW * 32) colst[q] = make_uint2(0u, 0u);
   for (int q = tid; q < R * D; q += NW * 32) rowst[q] = make_uint2(0u, 0u);
@@ -105,16 +188,18 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(double));
+  const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(F));
   if (tid == 0) {
-    const double* src;
-    col_window_src(a.s, i0 + (int64_t)xfirst * D, &src);
+    const F* src;
+    col_window_src(gs, i0 + (int64_t)xfirst * D, &src);
     mbar_expect_tx_arrive(&bar[0], col_bytes);
     tma_load_1d(smem + L.off_col0, src, col_bytes, &bar[0]);
   }
 
   RunState st[R];  // diagonal run state of the current (band, slot) segment
   double win[R][kW > 0 ? kW : 1];
+  unsigned long long win2[RP][kW > 0 ? kW : 1];  // packed f32 term windows (kPacked)
+  unsigned long long mism = 0;                   // fp32 mode: mismatched cells
   uint32_t ph_lo[R], ph_hi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -131,22 +216,40 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     const int buf = it & 1;
     const bool warm = x < xa;             // column lower parts only
     if (tid == 0 && x + 1 < xb) {
-      const double* src;
-      col_window_src(a.s, i0 + kx + D, &src);
+      const F* src;
+      col_window_src(gs, i0 + kx + D, &src);
       mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes);
       tma_load_1d(smem + (buf ? L.off_col0 : L.off_col1), src, col_bytes, &bar[buf ^ 1]);
     }
     mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
-    const int co = (int)((((uintptr_t)(a.s + i0 + kx)) >> 3) & 1);
-    const double* s_col =
-        reinterpret_cast<const double*>(smem + (buf ? L.off_col1 : L.off_col0)) + co + delta;
+    const int co = (int)((((uintptr_t)(gs + i0 + kx)) & 15u) / sizeof(F));
+    const F* s_col =
+        reinterpret_cast<const F*>(smem + (buf ? L.off_col1 : L.off_col0)) + co + delta;
 
     // term windows: every slot at the unit's first iteration, slot 0 afterwards
+    if constexpr (kPacked) {
+#pragma unroll
+      for (int u = 0; u < kW; ++u) {
+#pragma unroll
+        for (int pr = 0; pr < RP; ++pr) {
+          if (pr == 0 || x == xfirst) {
+            const float2 rv = s_row2[pr * PS + u];
+            const float cv = s_col[u];
+            const float d0 = __fsub_rn(rv.x, cv), d1 = __fsub_rn(rv.y, cv);
+            const float t0 = kSquare ? __fmul_rn(d0, d0) : fabsf(d0);
+            const float t1 = kSquare ? __fmul_rn(d1, d1) : fabsf(d1);
+            // slot 0 is refreshed; slot 1 keeps what it inherited from slot 0
+            win2[pr][u] = (x == xfirst) ? f2_pack(t0, t1)
+                                        : f2_pack(t0, f2_hi(win2[pr][u]));
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       st[r] = RunState{0u, 0u};  // every (band, slot) is a segment of its own
       if (r == 0 || x == xfirst) {
-        if constexpr (!kDirect && kW > 0) {
+        if constexpr (!kDirect && kW > 0 && !kPacked) {
           if constexpr (kLinfAnd) {
             uint32_t p = 0;
 #pragma unroll
@@ -178,13 +281,71 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 
     for (int c = 0; c < NCH; ++c) {
       uint32_t dw[R];
+      float amb[R];  // f32 filter: min |acc32 - c32| over the word (per pair when packed)
 #pragma unroll
-      for (int r = 0; r < R; ++r) dw[r] = 0u;
-      const double* colc = s_col + 32 * c;
-      const double* rowc = s_row + 32 * c;
+      for (int r = 0; r < R; ++r) {
+        dw[r] = 0u;
+        amb[r] = __int_as_float(0x7f800000);
+      }
+      const F* colc = s_col + 32 * c;
+      const F* rowc = s_row + 32 * c;
+      if constexpr (kPacked) {
+        const unsigned long long negc = f2_pack(-a.c32, -a.c32);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float cv = colc[t + kW];
+          const unsigned long long negcv = f2_pack(-cv, -cv);
+#pragma unroll
+          for (int pr = 0; pr < RP; ++pr) {
+            const float2 rv = s_row2[pr * PS + 32 * c + t + kW];
+            const unsigned long long d = f2_add(f2_pack(rv.x, rv.y), negcv);
+            const unsigned long long term = kSquare ? f2_mul(d, d) : (d & 0x7fffffff7fffffffull);
+            unsigned long long acc = win2[pr][0];
+#pragma unroll
+            for (int k = 1; k < M - 1; ++k) acc = f2_add(acc, win2[pr][k * TAU]);
+            acc = f2_add(acc, term);
+            const unsigned long long xx = f2_add(acc, negc);
+            // sign of acc32 - c32 (exact) shifted in; bit t ends at 31 - t
+            dw[2 * pr] = __funnelshift_l(__float_as_uint(f2_lo(xx)), dw[2 * pr], 1);
+            dw[2 * pr + 1] = __funnelshift_l(__float_as_uint(f2_hi(xx)), dw[2 * pr + 1], 1);
+            amb[pr] = fminf(amb[pr], fminf(fabsf(f2_lo(xx)), fabsf(f2_hi(xx))));
+#pragma unroll
+            for (int j = 0; j + 1 < kW; ++j) win2[pr][j] = win2[pr][j + 1];
+            win2[pr][kW - 1] = term;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) dw[r] = __brev(dw[r]);
+      } else
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        if constexpr (!kDirect) {
+        if constexpr (kF32) {  // direct f32 evaluation (runtime m, tau)
+          const int m = a.m, tau = a.tau;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float* rp = reinterpret_cast<const float*>(rowc) + r * HS + t;
+            const float* cp = reinterpret_cast<const float*>(colc) + t;
+            bool hit;
+            if (METRIC == kLinf || m == 1) {
+              hit = true;
+              for (int k = 0; k < m; ++k) {
+                const float ad = fabsf(__fsub_rn(rp[k * tau], cp[k * tau]));
+                hit &= ad <= a.thr32;
+                amb[r] = fminf(amb[r], fabsf(__fsub_rn(ad, a.c32)));
+              }
+            } else {
+              float acc = 0.0f;
+              for (int k = 0; k < m; ++k) {
+                const float d = __fsub_rn(rp[k * tau], cp[k * tau]);
+                const float term = (METRIC == kL2) ? __fmul_rn(d, d) : fabsf(d);
+                acc = (k == 0) ? term : __fadd_rn(acc, term);
+              }
+              hit = acc <= a.thr32;
+              amb[r] = fminf(amb[r], fabsf(__fsub_rn(acc, a.c32)));
+            }
+            if (hit) dw[r] |= 1u << t;
+          }
+        } else if constexpr (!kDirect) {
           const double cv = colc[t + kW];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -233,6 +394,27 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
       }
 
+      if constexpr (kF32) {
+        // words with a cell inside the band: float64 bits (exact mode) or the
+        // float32 bits plus the fp32/fp64 mismatch count (fp32 mode)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float am = kPacked ? amb[r / 2] : amb[r];
+          if (a.all_amb || am <= a.band32) {
+            const int kd = kdr[r];
+            const uint2 w = f32_recheck<METRIC>(a, i0 + r * HS + 32 * c, (int64_t)kd);
+            if (a.prec_mode == 0) {
+              dw[r] = w.x;
+            } else {
+              dw[r] = w.y;
+              if (!warm && kd >= theiler && kd < nrem) {
+                const uint32_t mk = low_mask(min(max(lastc[r] - 32 * c, 0), 32));
+                mism += (unsigned long long)((kd == 0) ? 1 : 2) * __popc((w.x ^ w.y) & mk);
+              }
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         uint32_t word;
@@ -400,9 +582,19 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           diag_finish(st[r], true, Pslot[r] + kd, Sslot[r] + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
       }
     }
+    if constexpr (kPacked) {  // slot r+1 continues slot r's window (pairs: lo = even slot)
+#pragma unroll
+      for (int j = 0; j < kW; ++j) {
+#pragma unroll
+        for (int pr = RP - 1; pr >= 0; --pr) {
+          const uint32_t lo_new = pr > 0 ? (uint32_t)(win2[pr - 1][j] >> 32) : 0u;
+          win2[pr][j] = ((unsigned long long)(uint32_t)win2[pr][j] << 32) | lo_new;
+        }
+      }
+    }
 #pragma unroll
     for (int r = R - 1; r >= 1; --r) {
-      if constexpr (!kDirect && kW > 0) {
+      if constexpr (!kDirect && kW > 0 && !kPacked) {
         if constexpr (kLinfAnd) {
           ph_lo[r] = ph_lo[r - 1];
         } else {
@@ -438,6 +630,11 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) pts64 += __shfl_xor_sync(0xffffffffu, pts64, o);
   if (lane == 0 && pts64) atomicAdd(a.points, pts64);
+  if constexpr (kF32) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
+    if (lane == 0 && mism) atomicAdd(a.mism, mism);
+  }
   __syncthreads();
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
     const uint32_t cnt = sh_hist[q];

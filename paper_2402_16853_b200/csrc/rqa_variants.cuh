@@ -12,6 +12,7 @@ struct Variant {
   int nw, r;              // warps per CTA, stacked slots (band = r * 32 * nw rows)
   int w;                  // term window (m-1)*tau
   int reuse;              // 1: compile-time (m, tau) with term reuse; 0: direct
+  int prec;               // 0: float64 evaluation; 1: f32 filter (rqa_unit.cuh)
   size_t smem;            // dynamic shared memory bytes
   cudaError_t (*launch)(const UnitArgs&, int nunits, int w, cudaStream_t);
   const void* kernel;     // for occupancy queries
@@ -19,28 +20,30 @@ struct Variant {
   int64_t slot_rows() const { return (int64_t)32 * nw; }
 };
 
-// 2 CTAs per SM, except the one-slot large-window variants (registers).
+// 2 CTAs per SM, except the one-slot (pair) large-window variants (registers).
 template <int M, int TAU, int NW, int R>
 constexpr int min_blocks() {
-  return (R == 1 && M > 0 && (M - 1) * TAU > 16) ? 1 : (NW == 4 ? 4 : (R == 2 ? 3 : 2));
+  return (R <= 2 && M > 0 && (M - 1) * TAU > 16) ? 1 : (NW == 4 ? 4 : (R == 2 ? 3 : 2));
 }
 
-template <int METRIC, int M, int TAU, int NW, int R>
+template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
-  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU);
-  auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>;
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC ? 4 : 8);
+  auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(), PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   k<<<nunits, NW * 32, L.total, st>>>(a, w);
   return cudaGetLastError();
 }
 
-template <int METRIC, int M, int TAU, int NW, int R>
+template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const SymSmem L(NW, R, w);
-  return Variant{NW, R, w, M == 0 ? 0 : 1, L.total, &launch_unit<METRIC, M, TAU, NW, R>,
-                 (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>()>};
+  const SymSmem L(NW, R, w, PREC ? 4 : 8);
+  return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total,
+                 &launch_unit<METRIC, M, TAU, NW, R, PREC>,
+                 (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(),
+                                           PREC>};
 }
 
 // Implemented in rqa_kernels_<metric>[_small].cu (one translation unit each so
@@ -52,6 +55,16 @@ bool find_variant_l2(int m, int tau, bool small, Variant* out);
 bool find_variant_linf(int m, int tau, bool small, Variant* out);
 bool find_variant_m1(int m, int tau, bool small, Variant* out);
 bool find_variant_direct(int metric, int m, int tau, bool small, Variant* out);
+// f32 filter kernels (PREC = 1): packed L1/L2 term reuse, else direct.
+bool find_variant_f32_l1(int m, int tau, Variant* out);
+bool find_variant_f32_l2(int m, int tau, Variant* out);
+bool find_variant_f32_direct(int metric, int m, int tau, Variant* out);
+
+inline bool find_variant_f32(int metric, int m, int tau, bool packed_only, Variant* out) {
+  if (m >= 2 && metric == kL1 && find_variant_f32_l1(m, tau, out)) return true;
+  if (m >= 2 && metric == kL2 && find_variant_f32_l2(m, tau, out)) return true;
+  return !packed_only && find_variant_f32_direct(metric, m, tau, out);
+}
 
 // Rows below which the 256-row geometry is chosen.  Work units balance the
 // SMs for any n, so the 1024-row geometry is used everywhere by default.

@@ -37,6 +37,11 @@ def default_workers() -> int:
         return os.cpu_count() or 1
 
 
+# precision keyword -> C-ABI code (rqa_run_prec); evaluation path reported in timing
+PRECISIONS = {"fp64": 64, "fp32": 32}
+EVALUATION_PATHS = {-1: "fp64", 0: "f32-filter", 1: "fp32"}
+
+
 def device_count() -> int:
     return int(_native.lib().rqa_device_count())
 
@@ -56,13 +61,21 @@ def _series_array(embedded: EmbeddedSeries) -> np.ndarray:
 
 def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
                  tile_size: int = DEFAULT_TILE_SIZE, workers: int | None = None, *,
-                 device: int = 0):
+                 device: int = 0, precision: str = "fp64"):
     """Full analysis on one B200; returns (LineHistograms, timing dict).
+
+    Mirrors run_analysis (engine.py:215-280): same arguments and validation;
+    tile_size / workers do not change the results (as in the reference).
+    ``precision``: "fp64" (default) is bit-exact against the float64
+    reference; "fp32" evaluates with float32 samples, arithmetic and radius
+    and reports ``timing["mismatched_cells"]``, the number of cells of the
+    full N x N matrix whose decision differs from the float64 one.
 
     timing keeps the reference keys (create_recurrence_matrix holds the fused
     kernel time, the two detector phases are fused into it and report 0.0)
     and adds h2d, fold, d2h, device_total, cells_per_second, band_rows,
-    bands.  Multi-GPU runs go through ``paper_2402_16853_b200.distributed``.
+    bands, evaluation ("fp64", "f32-filter" or "fp32"), f32_band.
+    Multi-GPU runs go through ``paper_2402_16853_b200.distributed``.
     """
     if workers is None:
         workers = default_workers()
@@ -70,6 +83,8 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         raise InvalidArgument("workers must be >= 1")  # engine.py:231-232
     if tile_size < 1:
         raise InvalidArgument("tile_size must be >= 1")  # engine.py:123-124
+    if precision not in PRECISIONS:
+        raise InvalidArgument(f"precision must be one of {sorted(PRECISIONS)}")
     if (embedded.embedding_dimension != settings.embedding_dimension
             or embedded.time_delay != settings.time_delay):
         raise InvalidArgument("embedded series and settings disagree on m / tau")
@@ -80,15 +95,17 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     vert = np.zeros(n + 1, np.int64)
     white = np.zeros(n + 1, np.int64)
     pts = np.zeros(1, np.int64)
+    mism = np.zeros(1, np.int64)
     tim = np.zeros(_native.TIMING_SLOTS, np.float64)
     p64 = ctypes.POINTER(ctypes.c_int64)
-    _native.call("rqa_run",
+    _native.call("rqa_run_prec",
                  s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0],
                  settings.embedding_dimension, settings.time_delay,
                  METRIC_CODES[settings.metric], float(settings.radius),
-                 settings.theiler_window, int(device),
+                 settings.theiler_window, PRECISIONS[precision], int(device),
                  diag.ctypes.data_as(p64), vert.ctypes.data_as(p64),
                  white.ctypes.data_as(p64), pts.ctypes.data_as(p64),
+                 mism.ctypes.data_as(p64),
                  tim.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     hist = LineHistograms(n, int(pts[0]), diag, vert, white)
     timing = {
@@ -102,6 +119,10 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         "cells_per_second": float(tim[5]),
         "band_rows": int(tim[6]),
         "bands": int(tim[7]),
+        "evaluation": EVALUATION_PATHS.get(int(tim[8]), "fp64"),
+        "f32_band": float(tim[9]),
         "total": time.perf_counter() - started,
     }
+    if precision == "fp32":
+        timing["mismatched_cells"] = int(mism[0])
     return hist, timing

@@ -1,0 +1,145 @@
+"""Precision paths of the CUDA engine (rqa_run_prec, SURVEY.md 8b `precision=`).
+
+* fp32 mode: histograms bit-identical to the oracle's float32 restatement
+  (numpy float32 semantics, oracle/rqa_oracle.c recurrence_tile32) and the
+  mismatched-cell count identical to the oracle's cell-by-cell comparison of
+  the float32 and float64 matrices.
+* fp64 through the f32 filter (float32 evaluation inside a certified band,
+  float64 re-evaluation of every word with a cell near the threshold): the
+  histograms must be bit-identical to the float64 oracle, including inputs
+  that make the band wide (forced with RQA_FILTER=2 in a subprocess).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from fixtures import assert_same
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gpu_available():
+    try:
+        from paper_2402_16853_b200 import _native
+
+        return _native.lib().rqa_device_count() > 0
+    except Exception:
+        return False
+
+
+if not _gpu_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2402_16853_b200 import AnalysisSettings, embed, run_analysis  # noqa: E402
+
+
+def _series(kind, length, rng):
+    if kind == "uniform":
+        return rng.uniform(0, 1, length)
+    if kind == "offset":   # float32 rounding of the samples decides many cells
+        return 100.0 + rng.uniform(0, 1e-3, length)
+    if kind == "sine":
+        return np.sin(np.linspace(0, 40 * np.pi, length)) + 0.05 * rng.normal(size=length)
+    if kind == "nan":
+        s = rng.uniform(0, 1, length)
+        s[[3, length // 2, length // 2 + 1]] = np.nan
+        return s
+    if kind == "huge":     # beyond the certifiable band: every word re-evaluated
+        return rng.uniform(0, 1, length) * 1e17
+    raise ValueError(kind)
+
+
+FP32_CASES = [
+    # (kind, length, m, tau, metric, radius, theiler)
+    ("uniform", 3000, 3, 1, "l2", 0.1, 0),        # packed f32x2 L2 reuse
+    ("uniform", 2500, 3, 2, "l1", 0.3, 1),        # packed L1 reuse
+    ("sine", 2200, 2, 1, "l2", 0.2, 0),
+    ("sine", 3001, 10, 5, "l1", 2.0, 10),         # packed, one slot pair (large window)
+    ("uniform", 2000, 1, 1, "l2", 0.01, 0),       # direct f32 (m = 1)
+    ("uniform", 2100, 3, 1, "linf", 0.1, 0),      # direct f32 L-inf
+    ("uniform", 1900, 6, 3, "l2", 0.6, 2),        # direct f32, runtime (m, tau)
+    ("offset", 2600, 2, 1, "l2", 2e-4, 0),        # many fp32/fp64 mismatches
+    ("offset", 2600, 3, 1, "l1", 4e-4, 0),
+    ("offset", 2600, 3, 1, "linf", 2e-4, 1),
+    ("nan", 1500, 3, 1, "l2", 0.2, 0),            # non-finite: all words re-evaluated
+    ("huge", 1200, 2, 1, "l2", 2e16, 0),
+]
+
+
+@pytest.mark.parametrize("case", FP32_CASES,
+                         ids=[f"{c[0]}-{c[1]}-m{c[2]}t{c[3]}-{c[4]}" for c in FP32_CASES])
+def test_fp32_mode_matches_oracle(case, oracle_lib):
+    kind, length, m, tau, metric, radius, w = case
+    rng = np.random.default_rng(length + 7 * m)
+    s = _series(kind, length, rng)
+    st = AnalysisSettings(m, tau, metric, radius, theiler_corrector=w)
+    h, timing = run_analysis(embed(s, m, tau), st, precision="fp32")
+    d, v, wh, p, mism = oracle_lib.oracle_histograms_prec(s, m, tau, metric, radius, w,
+                                                          precision=32, tile_size=256)
+    assert_same((h.diagonal, h.vertical, h.white_vertical, h.recurrence_points),
+                (d, v, wh, p), str(case))
+    assert timing["evaluation"] == "fp32"
+    assert timing["mismatched_cells"] == mism, (case, timing["mismatched_cells"], mism)
+    if kind == "offset":
+        assert mism > 0  # the case must exercise the mismatch count
+
+
+def test_fp32_mode_known_answers():
+    """Exact data (small integers): float32 and float64 agree everywhere."""
+    s = np.arange(400, dtype=np.float64) % 17
+    st = AnalysisSettings(2, 1, "l2", 3.0)
+    h32, t32 = run_analysis(embed(s, 2, 1), st, precision="fp32")
+    h64, _ = run_analysis(embed(s, 2, 1), st)
+    assert t32["mismatched_cells"] == 0
+    assert h32 == h64
+
+
+def test_default_fp64_path_is_float64():
+    rng = np.random.default_rng(5)
+    s = rng.uniform(0, 1, 5000)
+    _, timing = run_analysis(embed(s, 3, 1), AnalysisSettings(3, 1, "l2", 0.1))
+    assert timing["evaluation"] in ("fp64", "f32-filter")
+    if "RQA_FILTER" not in os.environ:
+        assert timing["evaluation"] == "fp64"
+
+
+_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2402_16853_b200 import AnalysisSettings, embed, run_analysis
+from oracle.oracle import oracle_histograms
+out = []
+rng = np.random.default_rng(17)
+for kind, m, tau, metric, r in (("offset", 2, 1, "l2", 2e-4), ("offset", 3, 2, "l1", 5e-4),
+                                ("uniform", 3, 1, "l2", 0.1), ("uniform", 4, 1, "l1", 0.4),
+                                ("uniform", 10, 5, "l2", 1.2)):
+    s = 100.0 + rng.uniform(0, 1e-3, 2400) if kind == "offset" else rng.uniform(0, 1, 2400)
+    h, t = run_analysis(embed(s, m, tau), AnalysisSettings(m, tau, metric, r))
+    d, v, w, p = oracle_histograms(s, m, tau, metric, r, 0, tile_size=512)
+    ok = (h.recurrence_points == p and (h.diagonal == d).all() and (h.vertical == v).all()
+          and (h.white_vertical == w).all())
+    out.append([kind, m, tau, metric, bool(ok), t["evaluation"]])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("mode,expect", [("2", "f32-filter"), ("0", "fp64"), ("1", None)])
+def test_filter_modes_in_subprocess(mode, expect):
+    """RQA_FILTER=1 uses the filter for narrow bands, 2 for every certifiable
+    band, 0 never; every path must reproduce the float64 oracle bit for bit."""
+    env = dict(os.environ, RQA_FILTER=mode)
+    out = subprocess.run([sys.executable, "-c", _CHILD, REPO], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rows = json.loads(out.stdout.strip().splitlines()[-1])
+    for kind, m, tau, metric, ok, ev in rows:
+        assert ok, (kind, m, tau, metric, ev)
+        want = expect or ("f32-filter" if kind == "uniform" else "fp64")
+        assert ev == want, (kind, m, tau, metric, ev)
