@@ -284,13 +284,14 @@ def main():
     d2h = 3 * (n + 1) * 8 + 8
     if world == 1:
         emb = embed(series_np, settings.embedding_dimension, settings.time_delay)
-        run_analysis(emb, settings)
+        dev_index = torch.cuda.current_device()
+        run_analysis(emb, settings, device=dev_index)
         e2e_t = []
         for _ in range(max(1, min(args.steps, 3))):
             flush_l2(flush)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            run_analysis(emb, settings)
+            run_analysis(emb, settings, device=dev_index)
             e2e_t.append(time.perf_counter() - t0)
         e2e_val = cells / float(np.mean(e2e_t))
     else:

@@ -95,6 +95,22 @@ int rqa_run_prec(const double *series, int64_t len, int32_t m, int32_t tau, int3
                  int64_t *mismatches, double *timing, char *err, size_t errlen);
 
 /*
+ * Single-process multi-GPU analysis (run_analysis(devices=[...])): the rows
+ * are split into n_devices equal-area stripes of the upper triangle, one host
+ * thread per stripe runs it on devices[g] (a device may appear more than
+ * once), the stripe summaries are gathered on devices[0] by peer copies
+ * (NVLink) and stitched there (rqa_stitch_device semantics); histograms and
+ * counts are summed.  Results are identical to rqa_run_prec for every device
+ * list.  n_devices == 1 is rqa_run_prec.  Timing: [1] slowest stripe's
+ * kernels, [2] stitch, [4] wall, [5] cells/s over the wall, [7] stripes.
+ */
+int rqa_run_multi(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                  double radius, int64_t theiler, int32_t precision, const int32_t *devices,
+                  int32_t n_devices, int64_t *diag, int64_t *vert, int64_t *white,
+                  int64_t *points, int64_t *mismatches, double *timing, char *err,
+                  size_t errlen);
+
+/*
  * Device-resident variant for callers that own device memory and a stream
  * (torch tensors): rows [row_lo, row_hi) of the recurrence matrix.
  *   mode 0 (final): rows must be [0, n); d_hist (int64[3*(n+1)], rows diag,

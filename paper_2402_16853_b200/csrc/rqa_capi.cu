@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/rqa_b200.h"
@@ -93,18 +95,25 @@ struct Workspace {
   size_t maxbits_cap = 0;
   int64_t* bounds = nullptr;
   size_t bounds_cap = 0;
+  int32_t* gather = nullptr;   // multi-device: gathered stripe summaries (device 0 only)
+  size_t gather_cap = 0;
   cudaEvent_t ev[6] = {};
   bool init = false;
 };
 
 std::mutex g_ws_mu;
-std::vector<Workspace*> g_ws;
+std::vector<Workspace*> g_ws;        // [slot * kMaxDevices + device]
+constexpr int kMaxDevices = 64;      // per-process device ids
+constexpr int kMaxSlots = 64;        // stripes of one multi-device call on the same device
 
-Workspace* workspace(int dev) {
+// Workspace of (device, slot): slot > 0 only for the extra stripes a
+// multi-device call places on a device it already uses.
+Workspace* workspace(int dev, int slot = 0) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if ((int)g_ws.size() <= dev) g_ws.resize(dev + 1, nullptr);
-  if (!g_ws[dev]) g_ws[dev] = new Workspace();
-  return g_ws[dev];
+  const size_t key = (size_t)slot * kMaxDevices + (size_t)dev;
+  if (g_ws.size() <= key) g_ws.resize(key + 1, nullptr);
+  if (!g_ws[key]) g_ws[key] = new Workspace();
+  return g_ws[key];
 }
 
 template <typename T>
@@ -552,6 +561,56 @@ __global__ void fp64_peak_kernel(double* out, int iters, double a) {
 
 }  // namespace
 
+// One stripe of a multi-device call, run by its own host thread.
+struct StripeJob {
+  int dev = 0, slot = 0;
+  int64_t lo = 0, hi = 0;
+  Workspace* ws = nullptr;
+  unsigned long long* hist = nullptr;  // [3(n+1) + 2]: histograms, points, mismatches
+  int32_t *pre = nullptr, *suf = nullptr;
+  uint32_t *col = nullptr, *row = nullptr;
+  float ms = 0.f;
+  int rc = 0;
+  char err[256] = {0};
+};
+
+int run_stripe_job(StripeJob* j, const Problem& p0, const double* series) {
+  char* err = j->err;
+  const size_t errlen = sizeof j->err;
+  RQA_CUDA(cudaSetDevice(j->dev), "cudaSetDevice");
+  Workspace* ws = j->ws;
+  if (!ws->init) {
+    RQA_CUDA(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : ws->ev) RQA_CUDA(cudaEventCreate(&e), "event");
+    ws->init = true;
+  }
+  cudaStream_t st = ws->stream;
+  Problem p = p0;
+  const size_t hn = (size_t)(p.n + 1), n = (size_t)p.n;
+  RQA_CUDA(grow(&ws->hist, &ws->hist_cap, 3 * hn + 2), "allocating histograms");
+  RQA_CUDA(grow(&ws->stripe_buf, &ws->stripe_buf_cap, 6 * n), "allocating stripe summaries");
+  j->hist = ws->hist;
+  j->pre = ws->stripe_buf;
+  j->suf = j->pre + n;
+  j->col = reinterpret_cast<uint32_t*>(j->suf + n);
+  j->row = j->col + 2 * n;
+  int rc = stage_series(ws, p, series, cudaMemcpyHostToDevice, st, err, errlen);
+  if (rc) return rc;
+  RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 2) * sizeof(unsigned long long), st), "memset");
+  RQA_CUDA(cudaMemsetAsync(j->row, 0, 2 * n * sizeof(uint32_t), st), "memset");
+  rc = plan_precision(ws, &p, st, err, errlen);
+  if (rc) return rc;
+  p.mism = ws->hist + 3 * hn + 1;
+  RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
+  rc = launch_rows(ws, p, j->lo, j->hi, kFoldStripe, ws->hist, ws->hist + 3 * hn, j->pre, j->suf,
+                   j->col, j->row, st, nullptr, err, errlen);
+  if (rc) return rc;
+  RQA_CUDA(cudaEventRecord(ws->ev[2], st), "event");
+  RQA_CUDA(cudaStreamSynchronize(st), "stripe kernels");
+  cudaEventElapsedTime(&j->ms, ws->ev[1], ws->ev[2]);
+  return RQA_OK;
+}
+
 void note_launch() { g_launches++; }
 
 }  // namespace rqa
@@ -653,6 +712,118 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
     timing[7] = (double)((p.n + p.var.band_rows() - 1) / p.var.band_rows());
     timing[8] = (double)p.filt;
     timing[9] = (double)p.band32;
+  }
+  return RQA_OK;
+}
+
+int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
+                  double radius, int64_t theiler, int32_t precision, const int32_t* devices,
+                  int32_t n_devices, int64_t* diag, int64_t* vert, int64_t* white,
+                  int64_t* points, int64_t* mismatches, double* timing, char* err,
+                  size_t errlen) {
+  if (!series || !diag || !vert || !white || !points || !devices)
+    return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
+  if (precision != 64 && precision != 32)
+    return set_err(err, errlen, "precision must be 64 or 32"), RQA_EINVAL;
+  if (n_devices < 1 || n_devices > kMaxSlots)
+    return set_err(err, errlen, "n_devices must be in [1, %d]", kMaxSlots), RQA_EINVAL;
+  Problem p;
+  int rc = validate(len, m, tau, metric, radius, theiler, &p, err, errlen);
+  if (rc) return rc;
+  p.precision = precision;
+  const int ndev = rqa_device_count();
+  if (ndev <= 0) return set_err(err, errlen, "no CUDA device available"), RQA_EDEVICE;
+  for (int g = 0; g < n_devices; ++g)
+    if (devices[g] < 0 || devices[g] >= ndev || devices[g] >= kMaxDevices)
+      return set_err(err, errlen, "device %d out of range (%d visible)", devices[g], ndev),
+             RQA_EINVAL;
+  if (n_devices == 1)
+    return rqa_run_prec(series, len, m, tau, metric, radius, theiler, precision, devices[0], diag,
+                        vert, white, points, mismatches, timing, err, errlen);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int G = n_devices;
+  const std::vector<int64_t> bounds = area_stripes(p.n, G, 1024);
+  std::vector<StripeJob> jobs(G);
+  for (int g = 0; g < G; ++g) {
+    jobs[g].dev = devices[g];
+    for (int q = 0; q < g; ++q) jobs[g].slot += devices[q] == devices[g];
+    jobs[g].lo = bounds[g];
+    jobs[g].hi = bounds[g + 1];
+    jobs[g].ws = workspace(jobs[g].dev, jobs[g].slot);
+  }
+  // every workspace is locked for the whole call (fixed order: no deadlock)
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int g = 0; g < G; ++g) locks.emplace_back(jobs[g].ws->mu);
+  {
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+      th.emplace_back([&, g] { jobs[g].rc = run_stripe_job(&jobs[g], p, series); });
+    for (auto& t : th) t.join();
+  }
+  for (int g = 0; g < G; ++g)
+    if (jobs[g].rc) return set_err(err, errlen, "device %d: %s", jobs[g].dev, jobs[g].err), jobs[g].rc;
+
+  // gather the stripe summaries on the first device and stitch there
+  StripeJob& j0 = jobs[0];
+  Workspace* ws0 = j0.ws;
+  RQA_CUDA(cudaSetDevice(j0.dev), "cudaSetDevice");
+  for (int g = 1; g < G; ++g)
+    if (jobs[g].dev != j0.dev) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, j0.dev, jobs[g].dev);
+      if (can && cudaDeviceEnablePeerAccess(jobs[g].dev, 0) != cudaSuccess) cudaGetLastError();
+    }
+  cudaStream_t st = ws0->stream;
+  const size_t n = (size_t)p.n, hn = n + 1;
+  RQA_CUDA(grow(&ws0->gather, &ws0->gather_cap, (size_t)G * 4 * n + 2 * n), "allocating gather");
+  int32_t* gpre = ws0->gather;
+  int32_t* gsuf = gpre + (size_t)G * n;
+  uint32_t* gcol = reinterpret_cast<uint32_t*>(gsuf + (size_t)G * n);
+  uint32_t* grow_ = gcol + (size_t)G * 2 * n;
+  std::vector<int64_t> hsum(3 * hn + 2, 0), hpart(3 * hn + 2);
+  for (int g = 0; g < G; ++g) {
+    const StripeJob& j = jobs[g];
+    RQA_CUDA(cudaMemcpyPeerAsync(gpre + g * n, j0.dev, j.pre, j.dev, n * 4, st), "gather");
+    RQA_CUDA(cudaMemcpyPeerAsync(gsuf + g * n, j0.dev, j.suf, j.dev, n * 4, st), "gather");
+    RQA_CUDA(cudaMemcpyPeerAsync(gcol + g * 2 * n, j0.dev, j.col, j.dev, 2 * n * 4, st), "gather");
+    if (j.hi > j.lo)
+      RQA_CUDA(cudaMemcpyPeerAsync(grow_ + 2 * j.lo, j0.dev, j.row + 2 * j.lo, j.dev,
+                                   (size_t)(j.hi - j.lo) * 2 * 4, st),
+               "gather");
+    RQA_CUDA(cudaSetDevice(j.dev), "cudaSetDevice");
+    RQA_CUDA(cudaMemcpy(hpart.data(), j.hist, (3 * hn + 2) * 8, cudaMemcpyDeviceToHost), "d2h");
+    RQA_CUDA(cudaSetDevice(j0.dev), "cudaSetDevice");
+    for (size_t q = 0; q < hsum.size(); ++q) hsum[q] += hpart[q];
+  }
+  // ws0->hist held stripe 0's partial histograms (copied above): reuse it
+  RQA_CUDA(cudaMemsetAsync(ws0->hist, 0, 3 * hn * sizeof(unsigned long long), st), "memset");
+  RQA_CUDA(cudaEventRecord(ws0->ev[3], st), "event");
+  rc = stitch_stripes(ws0, gpre, gsuf, gcol, grow_, bounds.data(), G, p.n, ws0->hist, st, err,
+                      errlen);
+  if (rc) return rc;
+  RQA_CUDA(cudaEventRecord(ws0->ev[4], st), "event");
+  RQA_CUDA(cudaMemcpyAsync(hpart.data(), ws0->hist, 3 * hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  RQA_CUDA(cudaStreamSynchronize(st), "stitch");
+  for (size_t q = 0; q < 3 * hn; ++q) hsum[q] += hpart[q];
+  memcpy(diag, hsum.data(), hn * 8);
+  memcpy(vert, hsum.data() + hn, hn * 8);
+  memcpy(white, hsum.data() + 2 * hn, hn * 8);
+  *points = hsum[3 * hn];
+  if (mismatches) *mismatches = hsum[3 * hn + 1];
+  if (timing) {
+    float stitch_ms = 0.f, kern_ms = 0.f;
+    cudaEventElapsedTime(&stitch_ms, ws0->ev[3], ws0->ev[4]);
+    for (const auto& j : jobs) kern_ms = std::max(kern_ms, j.ms);
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int q = 0; q < RQA_TIMING_SLOTS; ++q) timing[q] = 0.0;
+    timing[1] = kern_ms * 1e-3;
+    timing[2] = stitch_ms * 1e-3;
+    timing[4] = wall;
+    timing[5] = wall > 0 ? (double)p.n * (double)p.n / wall : 0.0;
+    timing[6] = 1024.0;
+    timing[7] = (double)G;
+    timing[8] = precision == 32 ? 1.0 : -1.0;
   }
   return RQA_OK;
 }
@@ -786,7 +957,8 @@ int rqa_release(void) {
   for (size_t d = 0; d < g_ws.size(); ++d) {
     Workspace* ws = g_ws[d];
     if (!ws) continue;
-    cudaSetDevice((int)d);
+    cudaSetDevice((int)(d % kMaxDevices));
+    cudaFree(ws->gather);
     cudaFree(ws->s_pad);
     cudaFree(ws->sf_pad);
     cudaFree(ws->maxbits);

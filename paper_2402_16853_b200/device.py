@@ -10,6 +10,8 @@ from dataclasses import dataclass
 from . import _native
 from .settings import METRIC_CODES, AnalysisSettings
 
+PRECISIONS = {"fp64": 64, "fp32": 32}
+
 __all__ = ["band_rows", "run_rows_device", "stitch_device", "StripeOutputs", "MODE_FINAL",
            "MODE_STRIPE"]
 
@@ -54,23 +56,26 @@ def _ptr(t):
 
 
 def run_rows_device(series, settings: AnalysisSettings, row_lo: int, row_hi: int, mode: int,
-                    hist, points, stripe: StripeOutputs | None = None, stream=None) -> None:
+                    hist, points, stripe: StripeOutputs | None = None, stream=None,
+                    precision: str = "fp64", mismatches=None) -> None:
     """Enqueue the band + fold kernels for rows [row_lo, row_hi) on ``stream``.
 
     series: float64 CUDA tensor of samples; hist: int64 CUDA tensor [3, n+1]
-    and points: int64 CUDA tensor [1], both accumulated into.
+    and points: int64 CUDA tensor [1], both accumulated into.  precision
+    "fp32" needs ``mismatches`` (int64 CUDA tensor [1], accumulated into).
     """
     import torch
 
     if stream is None:
         stream = torch.cuda.current_stream(series.device)
     so = stripe if stripe is not None else StripeOutputs(None, None, None, None)
-    _native.call("rqa_run_device", _ptr(series), series.numel(),
+    _native.call("rqa_run_device_prec", _ptr(series), series.numel(),
                  settings.embedding_dimension, settings.time_delay,
                  METRIC_CODES[settings.metric], float(settings.radius),
-                 settings.theiler_window, int(row_lo), int(row_hi), int(mode),
-                 _ptr(hist), _ptr(points), _ptr(so.prefix), _ptr(so.suffix), _ptr(so.col),
-                 _ptr(so.rowlead), ctypes.c_void_p(stream.cuda_stream))
+                 settings.theiler_window, PRECISIONS[precision], int(row_lo), int(row_hi),
+                 int(mode), _ptr(hist), _ptr(points), _ptr(mismatches), _ptr(so.prefix),
+                 _ptr(so.suffix), _ptr(so.col), _ptr(so.rowlead),
+                 ctypes.c_void_p(stream.cuda_stream))
 
 
 def stitch_device(gathered: StripeOutputs, bounds, n: int, hist, stream=None) -> None:

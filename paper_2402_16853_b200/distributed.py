@@ -41,17 +41,20 @@ def stripe_bounds(n: int, world: int, band: int) -> list:
     return out
 
 
-def gpu_stripe_fn(series_dev, settings, lo, hi, n, device):
-    """This rank's stripe on its GPU: (hist [3,n+1], points [1], StripeOutputs)."""
+def gpu_stripe_fn(series_dev, settings, lo, hi, n, device, precision="fp64"):
+    """This rank's stripe on its GPU: (hist [3,n+1], counts [2], StripeOutputs).
+
+    counts = (recurrence points, fp32/fp64 mismatched cells)."""
     import torch
 
     from .device import MODE_STRIPE, StripeOutputs, run_rows_device
 
     hist = torch.zeros(3, n + 1, dtype=torch.int64, device=device)
-    points = torch.zeros(1, dtype=torch.int64, device=device)
+    counts = torch.zeros(2, dtype=torch.int64, device=device)
     so = StripeOutputs.empty(n, device)
-    run_rows_device(series_dev, settings, lo, hi, MODE_STRIPE, hist, points, so)
-    return hist, points, so
+    run_rows_device(series_dev, settings, lo, hi, MODE_STRIPE, hist, counts[0:1], so,
+                    precision=precision, mismatches=counts[1:2])
+    return hist, counts, so
 
 
 def gpu_stitch_fn(gathered, bounds, n, hist):
@@ -115,11 +118,12 @@ def exchange(so, world, group=None):
 
 def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSettings, *,
                              group=None, device=None, band: int | None = None,
-                             stripe_fn=None, stitch_fn=None):
+                             stripe_fn=None, stitch_fn=None, precision: str = "fp64"):
     """Analysis over all ranks of ``group``; rank 0 returns LineHistograms.
 
     Other ranks return None.  ``device`` is this rank's torch device (default
-    cuda:LOCAL current device).
+    cuda:LOCAL current device).  With precision "fp32" the returned
+    histograms carry ``mismatched_cells`` (summed over the ranks).
     """
     import torch
     import torch.distributed as dist
@@ -130,7 +134,8 @@ def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSetting
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device())
     if stripe_fn is None:
-        stripe_fn = gpu_stripe_fn
+        def stripe_fn(*a):
+            return gpu_stripe_fn(*a, precision=precision)
     if stitch_fn is None:
         stitch_fn = gpu_stitch_fn
     if band is None:
@@ -147,4 +152,8 @@ def run_analysis_distributed(embedded: EmbeddedSeries, settings: AnalysisSetting
         return None
     stitch_fn(gathered, bounds, n, hist)
     h = hist.cpu().numpy()
-    return LineHistograms(n, int(points.cpu().item()), h[0].copy(), h[1].copy(), h[2].copy())
+    counts = points.cpu().numpy()
+    out = LineHistograms(n, int(counts[0]), h[0].copy(), h[1].copy(), h[2].copy())
+    if precision == "fp32":
+        out.mismatched_cells = int(counts[1]) if counts.shape[0] > 1 else 0
+    return out

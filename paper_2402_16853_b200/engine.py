@@ -61,11 +61,15 @@ def _series_array(embedded: EmbeddedSeries) -> np.ndarray:
 
 def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
                  tile_size: int = DEFAULT_TILE_SIZE, workers: int | None = None, *,
-                 device: int = 0, precision: str = "fp64"):
-    """Full analysis on one B200; returns (LineHistograms, timing dict).
+                 device: int | None = None, devices=None, precision: str = "fp64"):
+    """Full analysis on the B200s of this process; returns (LineHistograms, timing).
 
     Mirrors run_analysis (engine.py:215-280): same arguments and validation;
     tile_size / workers do not change the results (as in the reference).
+    ``devices``: CUDA device ids to split the rows over (one host thread per
+    device, stripes stitched on the first; a device may repeat); default: the
+    single ``device`` if given, else every visible GPU.  Results do not
+    depend on the device list.
     ``precision``: "fp64" (default) is bit-exact against the float64
     reference; "fp32" evaluates with float32 samples, arithmetic and radius
     and reports ``timing["mismatched_cells"]``, the number of cells of the
@@ -88,6 +92,11 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     if (embedded.embedding_dimension != settings.embedding_dimension
             or embedded.time_delay != settings.time_delay):
         raise InvalidArgument("embedded series and settings disagree on m / tau")
+    if devices is None:
+        devices = [device] if device is not None else list(range(max(1, device_count())))
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise InvalidArgument("devices must not be empty")
     started = time.perf_counter()
     s = _series_array(embedded)
     n = embedded.n_vectors
@@ -98,15 +107,18 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     mism = np.zeros(1, np.int64)
     tim = np.zeros(_native.TIMING_SLOTS, np.float64)
     p64 = ctypes.POINTER(ctypes.c_int64)
-    _native.call("rqa_run_prec",
-                 s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0],
-                 settings.embedding_dimension, settings.time_delay,
-                 METRIC_CODES[settings.metric], float(settings.radius),
-                 settings.theiler_window, PRECISIONS[precision], int(device),
-                 diag.ctypes.data_as(p64), vert.ctypes.data_as(p64),
-                 white.ctypes.data_as(p64), pts.ctypes.data_as(p64),
-                 mism.ctypes.data_as(p64),
-                 tim.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    args = (s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0],
+            settings.embedding_dimension, settings.time_delay,
+            METRIC_CODES[settings.metric], float(settings.radius),
+            settings.theiler_window, PRECISIONS[precision])
+    outs = (diag.ctypes.data_as(p64), vert.ctypes.data_as(p64), white.ctypes.data_as(p64),
+            pts.ctypes.data_as(p64), mism.ctypes.data_as(p64),
+            tim.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if len(devices) == 1:
+        _native.call("rqa_run_prec", *args, devices[0], *outs)
+    else:
+        dv = (ctypes.c_int32 * len(devices))(*devices)
+        _native.call("rqa_run_multi", *args, dv, len(devices), *outs)
     hist = LineHistograms(n, int(pts[0]), diag, vert, white)
     timing = {
         "create_recurrence_matrix": float(tim[1]),
@@ -120,6 +132,7 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         "band_rows": int(tim[6]),
         "bands": int(tim[7]),
         "evaluation": EVALUATION_PATHS.get(int(tim[8]), "fp64"),
+        "devices": devices,
         "f32_band": float(tim[9]),
         "total": time.perf_counter() - started,
     }
