@@ -172,6 +172,22 @@ int rqa_block(const double *series, int64_t len, int32_t m, int32_t tau, int32_t
               int64_t col1, int32_t factor, int32_t device, uint8_t *out, char *err,
               size_t errlen);
 
+/*
+ * Per-tile line detectors of the reference's operator API on the GPU
+ * (detect_diagonal_lines / detect_vertical_lines, engine.py:167-192 and the
+ * scans of :322-433, carry contract :287-319).  tile_bits: height x width
+ * bits, row-major, MSB first (np.packbits of the flattened tile).
+ *   kind 0: diagonals; carry_a = the tile's height+width-1 diagonal carries
+ *     (CarryoverBuffers.diagonal[(col0-row0) - (height-1) + n-1 ...]),
+ *     hist_a = LineHistograms.diagonal (n+1, accumulated into).
+ *   kind 1: columns; carry_a / carry_b = the width vertical / white-vertical
+ *     carries, hist_a / hist_b = vertical / white_vertical histograms.
+ * Carries are updated in place.  Dependency checks stay with the caller.
+ */
+int rqa_tile_scan(const uint8_t *tile_bits, int64_t height, int64_t width, int64_t n,
+                  int32_t kind, int64_t *carry_a, int64_t *carry_b, int64_t *hist_a,
+                  int64_t *hist_b, int32_t device, char *err, size_t errlen);
+
 /* FP64 pipe microbenchmark on `device`: sustained DADD and DMUL operations
  * per second (the roofline denominator of the FP64-bound band kernel). */
 int rqa_fp64_peak(int32_t device, double *dadd_per_s, double *dmul_per_s, char *err,

@@ -23,7 +23,13 @@ from .errors import InvalidArgument
 from .histograms import LineHistograms
 from .settings import METRIC_CODES, AnalysisSettings
 
-__all__ = ["DEFAULT_TILE_SIZE", "default_workers", "run_analysis", "device_count",
+from .operators import (CarryoverBuffers, Tile, TileGrid, create_recurrence_matrix,  # noqa: E402,F401
+                        detect_diagonal_lines, detect_vertical_lines, flush_carryovers,
+                        partition)
+
+__all__ = ["DEFAULT_TILE_SIZE", "TileGrid", "Tile", "CarryoverBuffers", "partition",
+           "create_recurrence_matrix", "detect_diagonal_lines", "detect_vertical_lines",
+           "flush_carryovers", "run_analysis", "default_workers", "device_count",
            "exact_threshold"]
 
 DEFAULT_TILE_SIZE = 4096  # engine.py:44 (accepted, validated, geometry is device-chosen)
