@@ -105,6 +105,9 @@ struct SymFoldArgs {
   uint2* out_col;
 };
 
+// Segments whose loads a fold thread issues together.
+constexpr int kFoldBatch = 8;
+
 // Block-local line histogram of the fold kernels: shared 32-bit bins for
 // lengths < kSmemBins (runs that cross segment edges are plentiful, e.g. one
 // white run per hook and band), flushed once per block.
@@ -143,21 +146,36 @@ __global__ void sym_fold_diag(const SymFoldArgs a, const int mode) {
     int64_t open = 0, pstr = -1;
     int64_t lo = a.row_lo, off = k, stride = n - a.row_lo;
     const int64_t nseg_k = min((int64_t)a.nb, (rows - a.row_lo + a.H - 1) / a.H);
-    for (int64_t g = 0; g < nseg_k; ++g) {
-      const int64_t hi = min(lo + a.H, a.row_hi);
-      const int64_t L = min(hi, rows) - lo;
-      const int64_t p = (int64_t)a.P[off];
-      if (p == L) {
-        open += L;
-      } else {
-        const int64_t x = open + p;
-        if (mode == kFoldStripe && pstr < 0) pstr = x;
-        else if (x > 0) h.add(kDiag, x, (uint32_t)wgt);
-        open = (hi <= rows) ? (int64_t)a.S[off] : 0;
+    // segments in batches: all loads of a batch are issued before the
+    // (sequential) monoid walk, so a thread keeps 2*kFoldBatch loads in flight
+    for (int64_t g0 = 0; g0 < nseg_k; g0 += kFoldBatch) {
+      uint16_t pv[kFoldBatch], sv[kFoldBatch];
+#pragma unroll
+      for (int q = 0; q < kFoldBatch; ++q) {
+        const int64_t oq = off + q * stride - a.H * (int64_t)(q * (q - 1) / 2);
+        const bool in = g0 + q < nseg_k;
+        pv[q] = in ? a.P[oq] : (uint16_t)0;
+        sv[q] = in ? a.S[oq] : (uint16_t)0;
       }
-      lo += a.H;
-      off += stride;
-      stride -= a.H;
+#pragma unroll
+      for (int q = 0; q < kFoldBatch; ++q) {
+        if (g0 + q < nseg_k) {
+          const int64_t hi = min(lo + a.H, a.row_hi);
+          const int64_t L = min(hi, rows) - lo;
+          const int64_t p = (int64_t)pv[q];
+          if (p == L) {
+            open += L;
+          } else {
+            const int64_t x = open + p;
+            if (mode == kFoldStripe && pstr < 0) pstr = x;
+            else if (x > 0) h.add(kDiag, x, (uint32_t)wgt);
+            open = (hi <= rows) ? (int64_t)sv[q] : 0;
+          }
+          lo += a.H;
+        }
+      }
+      off += kFoldBatch * stride - a.H * (int64_t)(kFoldBatch * (kFoldBatch - 1) / 2);
+      stride -= kFoldBatch * a.H;
     }
     if (mode == kFoldFinal) {
       if (open > 0) h.add(kDiag, open, (uint32_t)wgt);
@@ -301,19 +319,33 @@ __global__ void unit_fold_hooks(const UnitFoldArgs a, const int mode) {
     Seg acc{0u, 0u, 0u};
     {
       int64_t lo = a.row_lo, off = c - a.row_lo, stride = n - a.row_lo;
-      for (int g = 0; g < a.nb && lo < c; ++g) {
-        const int64_t hi = min(lo + a.H, a.row_hi);
-        const int64_t L = min(hi, c) - lo;
-        const uint32_t v = a.colsum[off];
-        const uint32_t top = v >> 16, bot = v & 0xffffu;
-        if ((int64_t)run_len(top) == L && acc.uniform && run_bit(top) == run_bit(acc.first)) {
-          acc.first = acc.last = acc.first + (uint32_t)(L << 1);  // uniform + uniform, same bit
-        } else {
-          acc = seg_combine(acc, Seg{top, bot, (int64_t)run_len(top) == L ? 1u : 0u}, h);
+      // bands above row c, loads batched as in sym_fold_diag
+      const int64_t nbc = c > a.row_lo ? min((int64_t)a.nb, (c - a.row_lo + a.H - 1) / a.H) : 0;
+      for (int64_t g0 = 0; g0 < nbc; g0 += kFoldBatch) {
+        uint32_t vv[kFoldBatch];
+#pragma unroll
+        for (int q = 0; q < kFoldBatch; ++q) {
+          // next band: offset grows by (n - lo_g), index shrinks by H
+          const int64_t oq = off + q * (stride - a.H) - a.H * (int64_t)(q * (q - 1) / 2);
+          vv[q] = g0 + q < nbc ? a.colsum[oq] : 0u;
         }
-        lo += a.H;
-        off += stride - a.H;   // next band: offset grows by (n - lo_g), index shrinks by H
-        stride -= a.H;
+#pragma unroll
+        for (int q = 0; q < kFoldBatch; ++q) {
+          if (g0 + q < nbc) {
+            const int64_t hi = min(lo + a.H, a.row_hi);
+            const int64_t L = min(hi, c) - lo;
+            const uint32_t v = vv[q];
+            const uint32_t top = v >> 16, bot = v & 0xffffu;
+            if ((int64_t)run_len(top) == L && acc.uniform && run_bit(top) == run_bit(acc.first)) {
+              acc.first = acc.last = acc.first + (uint32_t)(L << 1);  // uniform + uniform
+            } else {
+              acc = seg_combine(acc, Seg{top, bot, (int64_t)run_len(top) == L ? 1u : 0u}, h);
+            }
+            lo += a.H;
+          }
+        }
+        off += kFoldBatch * (stride - a.H) - a.H * (int64_t)(kFoldBatch * (kFoldBatch - 1) / 2);
+        stride -= kFoldBatch * a.H;
       }
     }
     // row part: pieces of row c (only if the row belongs to these bands)
