@@ -38,6 +38,11 @@ extern "C" {
 #define RQA_ESHORT (-2)
 #define RQA_EDEVICE (-3)
 #define RQA_ENOMEM (-4)
+#define RQA_EUNSUPPORTED (-5) /* rqa_read_column: input the native reader does not handle */
+#define RQA_EIO (-6)          /* rqa_read_column: FileNotReadable */
+#define RQA_ECOLUMN (-7)      /* rqa_read_column: ColumnOutOfRange */
+#define RQA_EPARSE (-8)       /* rqa_read_column: ParseError (token in err) */
+#define RQA_EEMPTY (-9)       /* rqa_read_column: EmptySeries */
 
 /* Number of timing slots written by rqa_run (seconds):
  * [0] h2d, [1] band kernel, [2] fold kernel, [3] d2h, [4] total device span,
@@ -192,6 +197,24 @@ int rqa_tile_scan(const uint8_t *tile_bits, int64_t height, int64_t width, int64
  * per second (the roofline denominator of the FP64-bound band kernel). */
 int rqa_fp64_peak(int32_t device, double *dadd_per_s, double *dmul_per_s, char *err,
                   size_t errlen);
+
+/*
+ * Native, multi-threaded read_column (ingest.py:53-129) for ASCII files:
+ * universal newlines, blank lines ignored, `offset` non-empty rows skipped
+ * unparsed, the token str.strip()ped and parsed like Python float()
+ * (underscores, inf/nan spellings), non-finite values rejected.  On success
+ * *values is a malloc'ed array of *count doubles (free with rqa_free) and
+ * *skipped the rows dropped by skip_invalid.  Errors: RQA_EIO, RQA_ECOLUMN
+ * (*err_line, *err_fields), RQA_EPARSE (*err_line, the token's bytes in err and
+ * their count in *err_fields), RQA_EEMPTY;
+ * RQA_EUNSUPPORTED for non-ASCII content or delimiters (use the Python
+ * reader).  threads <= 0: all hardware threads.
+ */
+int rqa_read_column(const char *path, char delimiter, int64_t column, int64_t offset,
+                    int32_t skip_invalid, int32_t threads, double **values, int64_t *count,
+                    int64_t *skipped, int64_t *err_line, int64_t *err_fields, char *err,
+                    size_t errlen);
+void rqa_free(void *p);
 
 /* Release cached device workspaces of this process. */
 int rqa_release(void);

@@ -48,6 +48,10 @@ SYMBOLS = {
                              _i32, _i32, _c.POINTER(_c.c_uint8), _c.c_char_p, _c.c_size_t]),
     "rqa_tile_scan": (_c.c_int, [_c.POINTER(_c.c_uint8), _i64, _i64, _i64, _i32, _pi64, _pi64,
                                  _pi64, _pi64, _i32, _c.c_char_p, _c.c_size_t]),
+    "rqa_read_column": (_c.c_int, [_c.c_char_p, _c.c_char, _i64, _i64, _i32, _i32,
+                                   _c.POINTER(_pd), _pi64, _pi64, _pi64, _pi64, _c.c_char_p,
+                                   _c.c_size_t]),
+    "rqa_free": (None, [_vp]),
     "rqa_fp64_peak": (_c.c_int, [_i32, _pd, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_release": (_c.c_int, []),
 }

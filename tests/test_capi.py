@@ -20,7 +20,7 @@ HEADER = os.path.join(REPO, "include", "rqa_b200.h")
 
 def header_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t)\s+\*?(rqa_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void)\s+\*?(rqa_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_expected_symbols():
