@@ -320,13 +320,24 @@ def main():
     local_cells = float(n - lo + n - hi) * float(hi - lo)
     alg_ops = local_cells * ops_per_cell(settings)
     achieved = alg_ops / t_kern
+    # dram bytes per launch of the dominant kernel from the committed ncu capture
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(args.workload)
+        if tr and world == 1:
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            traffic_src = "profiles/ncu_traffic.json (" + tr["kernel"] + ", ncu --set full)"
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {
         "bound": "fp64", "unit": "FP64 op/s",
         "achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
         "peak_source": "measured in-run: rqa_fp64_peak DADD/DMUL microbenchmark (not in "
                        "MEASURED_PEAKS.json, which has only HBM and bf16)",
-        "traffic": None,
-        "kernel": "band_kernel (fused test + runs + histograms) + fold, one launch pair",
+        "traffic": traffic,
+        "traffic_source": traffic_src,
+        "kernel": "unit_kernel (fused test + runs + histograms) + folds, one launch triple",
         "kernel_s": t_kern,
         "algorithmic_ops_per_cell": ops_per_cell(settings),
         "executed_fp64_ops_per_cell": executed_ops_per_cell(settings),

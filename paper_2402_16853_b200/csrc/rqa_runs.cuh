@@ -163,6 +163,7 @@ struct EventQueue {
   uint32_t head;     // warp-uniform
   uint32_t tail;     // warp-uniform
   uint32_t lt_mask;  // (1 << lane) - 1
+  uint32_t ring_sa;  // shared-window address of ring (set by the kernel)
 };
 
 // Expand whole groups of 32 events (all = true: everything left).  Kept out
@@ -206,9 +207,12 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
   st.first = mkfirst ? cur + (p1 << 1) : st.first;
   st.cur = ev ? cur_ev : cur + ((uint32_t)nb << 1);
   const uint32_t m = __ballot_sync(0xffffffffu, ev);
-  if (ev)
-    q.ring[(q.tail + __popc(m & q.lt_mask)) % kQueueCap] =
-        make_uint4(bnd, cur, (diag_weight << 1) | (mkfirst ? 1u : 0u), 0u);
+  if (ev) {  // 32-bit shared address: no generic-address rematerialisation per push
+    const uint32_t slot = (q.tail + __popc(m & q.lt_mask)) & (uint32_t)(kQueueCap - 1);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(q.ring_sa + 16u * slot),
+                 "r"(bnd), "r"(cur), "r"((diag_weight << 1) | (mkfirst ? 1u : 0u)), "r"(0u)
+                 : "memory");
+  }
   q.tail += __popc(m);
 }
 

@@ -162,6 +162,7 @@ sym_kernel(const SymArgs a, const int W_rt) {
   const Transposer tr(lane);
   EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
+  evq.ring_sa = smem_u32(evq.ring);
 
   for (int q = tid; q < 3 * kSmemBins; q += NW * 32) sh_hist[q] = 0u;
   for (int q = tid; q < H + W; q += NW * 32) s_row[q] = a.s[i0 + q];

@@ -159,6 +159,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   const Transposer tr(lane);
   EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
+  evq.ring_sa = smem_u32(evq.ring);
   uint16_t* Pslot[R];
   uint16_t* Sslot[R];
   const int64_t ptot = slot_offset((int64_t)((a.row_hi - a.row_lo + HS - 1) / HS), n, a.row_lo, HS);
@@ -530,17 +531,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           lim_new[p] = (do_new && x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
         }
         if (!(a.skip & 4) && x >= rs_[PR - 1]) {
-#pragma unroll 1
-          for (int c = NCH - 1; c >= 0; --c) {
-            if (c == wv) {
-#pragma unroll
-              for (int p = 0; p < PR; ++p) {
-                nst[p] = cur[p];
-                cur[p] = fin[p];
-              }
-            }
-            const bool finishing = c <= wv;
-            if (finishing ? !do_fin : !do_new) continue;
+          // column window c of slot rows: words of warps wp-1 and wp funnel-
+          // shifted into aligned columns, transposed, met bottom-up
+          auto col_step = [&](int c, const int* lim) {
             const int wp = (wv - c) & (NW - 1);
 #pragma unroll
             for (int p = 0; p < PR; ++p) {
@@ -548,11 +541,26 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               const uint32_t w1 = rowbuf[wp * H + lrow];
               const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
               const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
-              const int nb = min(max((finishing ? lim_fin[p] : lim_new[p]) - 32 * c, 0), 32);
+              const int nb = min(max(lim[p] - 32 * c, 0), 32);
               const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
               runs_push(bits, nb, cur[p], 0u, evq);
             }
             if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+          };
+          // windows above the warp's own start the columns of iteration x+1
+          if (do_new) {
+#pragma unroll 1
+            for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new);
+          }
+#pragma unroll
+          for (int p = 0; p < PR; ++p) {
+            nst[p] = cur[p];
+            cur[p] = fin[p];
+          }
+          // the warp's own window and those below finish the columns of x
+          if (do_fin) {
+#pragma unroll 1
+            for (int c = wv; c >= 0; --c) col_step(c, lim_fin);
           }
 #pragma unroll
           for (int p = 0; p < PR; ++p) fin[p] = cur[p];
