@@ -49,6 +49,27 @@ double threshold_for(int metric, int m, double radius) {
   return (metric == kL2 && m > 1) ? l2_threshold(radius) : radius;
 }
 
+// Prefilter bound D*: acc <= T forces every term <= T, i.e. |d| <= D* with
+// D* = max{x >= 0 : fl(x * x) <= T} for L2 (terms d*d), T for L1 (terms |d|).
+double prefilter_bound(int metric, double T) {
+  if (metric != kL2) return T;
+  if (!(T >= 0) || std::isinf(T)) return T;
+  // fl(x * x) is monotone in x >= 0, and so is the bit pattern of x: binary
+  // search the largest pattern whose square rounds to <= T (T = 0 included,
+  // where every x below ~2^-537 squares to 0)
+  uint64_t lo = 0, hi = 0x7ff0000000000000ull;  // fl(0*0) <= T; inf*inf > T
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    double x;
+    memcpy(&x, &mid, sizeof x);
+    if (x * x <= T) lo = mid;
+    else hi = mid;
+  }
+  double x;
+  memcpy(&x, &lo, sizeof x);
+  return x;
+}
+
 // fp32-mode threshold: T*32 = max{x : sqrtf(x) <= fl32(eps)} for L2 with
 // m > 1, else fl32(radius) (numpy float32 semantics, oracle/rqa_oracle.c).
 float threshold_for32(int metric, int m, double radius) {
@@ -141,6 +162,7 @@ struct Problem {
   int all_amb = 0;
   const float* sf = nullptr;
   unsigned long long* mism = nullptr;
+  double dstar = 0.0;   // prefilter bound (var.prec == 2)
 };
 
 int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
@@ -215,6 +237,24 @@ bool f32_band(const Problem& p, double maxabs, bool finite, float c32, float* ba
   if (!(B < 1e30)) return false;
   *band = std::nextafter((float)B, INFINITY);
   return true;
+}
+
+// Fraction of prefilter candidates on pseudo-random cells (i, j): all m
+// components within D*.  One thread per sample, counts into *hits.
+__global__ void sample_candidates_kernel(const double* __restrict__ s, int64_t n, int m, int tau,
+                                         double dstar, int samples, unsigned long long* hits) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= samples) return;
+  uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(q + 1);
+  h ^= h >> 31;
+  h *= 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 29;
+  const int64_t i = (int64_t)((h & 0xffffffffull) % (uint64_t)n);
+  const int64_t j = (int64_t)((h >> 32) % (uint64_t)n);
+  bool c = true;
+  for (int k = 0; k < m && c; ++k)
+    c = fabs(__dsub_rn(s[i + (int64_t)k * tau], s[j + (int64_t)k * tau])) <= dstar;
+  if (c) atomicAdd(hits, 1ull);
 }
 
 __global__ void prep_f32_kernel(const double* __restrict__ s, float* __restrict__ sf, int64_t count,
@@ -308,6 +348,42 @@ int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
   p->all_amb = 0;
   p->filt = 0;
   p->var = fv;
+  return RQA_OK;
+}
+
+// Sparse prefilter plan (precision 64, float64 kernels): sample the fraction
+// of cells whose m components all lie within D*; below kPrefilterMax the
+// prefilter kernel (AND of predicates + exact sums of the candidates) issues
+// fewer instructions than the term-window kernel.  RQA_PREFILTER=0 disables,
+// =1 forces it whenever a variant exists.  Results are identical either way.
+constexpr double kPrefilterMax = 0.05;
+
+int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
+  if (p->precision != 64 || p->filt != -1) return RQA_OK;
+  static const char* penv = getenv("RQA_PREFILTER");
+  const int want = penv ? atoi(penv) : 2;
+  if (want == 0) return RQA_OK;
+  Variant pv;
+  if (!find_variant_pre(p->metric, p->m, p->tau, &pv)) return RQA_OK;
+  const double dstar = prefilter_bound(p->metric, p->thr);
+  if (!(dstar >= 0) || std::isinf(dstar)) return RQA_OK;
+  if (want != 1) {
+    const int samples = 1 << 16;
+    RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 2), "allocating");
+    RQA_CUDA(cudaMemsetAsync(ws->maxbits + 1, 0, sizeof(unsigned long long), st), "memset");
+    sample_candidates_kernel<<<samples / 256, 256, 0, st>>>(ws->s_pad + p->pad, p->n, p->m,
+                                                           p->tau, dstar, samples,
+                                                           ws->maxbits + 1);
+    RQA_CUDA(cudaGetLastError(), "launching candidate sampling");
+    g_launches++;
+    unsigned long long hits = 0;
+    RQA_CUDA(cudaMemcpyAsync(&hits, ws->maxbits + 1, sizeof hits, cudaMemcpyDeviceToHost, st),
+             "d2h");
+    RQA_CUDA(cudaStreamSynchronize(st), "candidate sampling");
+    if ((double)hits / samples > kPrefilterMax) return RQA_OK;
+  }
+  p->dstar = dstar;
+  p->var = pv;
   return RQA_OK;
 }
 
@@ -430,6 +506,7 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.prec_mode = p.filt == 1 ? 1 : 0;
   a.all_amb = p.all_amb;
   a.mism = p.mism;
+  a.dstar = p.dstar;
   ua.units = ws->units;
   ua.rowpiece = ws->rowpiece;
   RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
@@ -599,6 +676,7 @@ int run_stripe_job(StripeJob* j, const Problem& p0, const double* series) {
   RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 2) * sizeof(unsigned long long), st), "memset");
   RQA_CUDA(cudaMemsetAsync(j->row, 0, 2 * n * sizeof(uint32_t), st), "memset");
   rc = plan_precision(ws, &p, st, err, errlen);
+  if (!rc) rc = plan_prefilter(ws, &p, st, err, errlen);
   if (rc) return rc;
   p.mism = ws->hist + 3 * hn + 1;
   RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
@@ -681,6 +759,7 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
   if (rc) return rc;
   RQA_CUDA(cudaMemsetAsync(ws->hist, 0, (3 * hn + 2) * sizeof(unsigned long long), st), "memset");
   rc = plan_precision(ws, &p, st, err, errlen);
+  if (!rc) rc = plan_prefilter(ws, &p, st, err, errlen);
   if (rc) return rc;
   p.mism = ws->hist + 3 * hn + 1;
   RQA_CUDA(cudaEventRecord(ws->ev[1], st), "event");
@@ -710,7 +789,7 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
     timing[5] = kern > 0 ? (double)p.n * (double)p.n / kern : 0.0;
     timing[6] = (double)p.var.band_rows();
     timing[7] = (double)((p.n + p.var.band_rows() - 1) / p.var.band_rows());
-    timing[8] = (double)p.filt;
+    timing[8] = p.var.prec == 2 ? 2.0 : (double)p.filt;
     timing[9] = (double)p.band32;
   }
   return RQA_OK;
@@ -870,6 +949,7 @@ int rqa_run_device_prec(const double* d_series, int64_t len, int32_t m, int32_t 
   rc = stage_series(ws, p, d_series, cudaMemcpyDeviceToDevice, st, err, errlen);
   if (rc) return rc;
   rc = plan_precision(ws, &p, st, err, errlen);
+  if (!rc) rc = plan_prefilter(ws, &p, st, err, errlen);
   if (rc) return rc;
   if (p.filt == 0 && !d_mismatches) {  // exact filter: counter unused but must exist
     RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 1), "allocating");

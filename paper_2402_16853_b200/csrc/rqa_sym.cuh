@@ -46,6 +46,7 @@ struct SymArgs {
   int prec_mode;             // 0: exact (ambiguous words take the float64 bits); 1: fp32 mode
   int all_amb;               // 1: every word is re-evaluated (band not certifiable)
   unsigned long long* mism;  // fp32 mode: cells whose fp32 and fp64 decisions differ
+  double dstar;              // prefilter (PREC 2): |d| <= dstar for every term of a candidate
 };
 
 // Compact per-band offset of entries kd (or c - i0) in [0, n - i0).

@@ -114,9 +114,17 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   constexpr bool kDirect = (M == 0);
   constexpr int kW = kDirect ? 0 : (M - 1) * TAU;
   constexpr bool kLinfAnd = (METRIC == kLinf) && (M >= 2);
+  // PREC 2: sparse prefilter for L1/L2 (exact).  Every term of a sum of
+  // non-negative terms is <= the float64 sum, so acc <= T implies
+  // |d_k| <= D* for every k (D* = max{x : fl(x*x) <= T} for L2, T for L1):
+  // the AND of the m shifted per-cell predicates |d| <= D* (as for L-inf)
+  // marks the only cells that can be recurrent, and only those are summed.
+  constexpr bool kPre = (PREC == 2) && (M >= 2) && (METRIC != kLinf);
+  constexpr bool kAnd = kLinfAnd || kPre;
   constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
   constexpr int NCH = HS / 32;  // == NW
-  static_assert(kLinfAnd ? kW <= 32 : kW <= 48, "term window too large");
+  static_assert(kAnd ? kW <= 32 : kW <= 48, "term window too large");
+  static_assert(PREC != 2 || kPre, "prefilter: L1/L2 term-reuse kernels only");
   constexpr bool kF32 = (PREC == 1);
   // packed f32x2 evaluation over slot pairs (2r, 2r+1): L1/L2 term reuse
   constexpr bool kPacked = kF32 && !kDirect && !kLinfAnd && M >= 2 && (R % 2 == 0);
@@ -150,6 +158,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   const int hrows = (int)(i_end - i0);
   const int theiler = (int)min(a.theiler, (int64_t)1 << 30);
   const double thr = a.thr;
+  const double athr = kPre ? a.dstar : thr;  // per-component predicate threshold
   const int xa = unit.xa, xb = unit.xb;
   const int xfirst = xa > 0 ? xa - 1 : 0;  // xa-1: recomputed for the columns finishing at xa
   const int64_t goff0 = b * R;              // global slot index of slot 0
@@ -251,11 +260,11 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       st[r] = RunState{0u, 0u};  // every (band, slot) is a segment of its own
       if (r == 0 || x == xfirst) {
         if constexpr (!kDirect && kW > 0 && !kPacked) {
-          if constexpr (kLinfAnd) {
+          if constexpr (kAnd) {
             uint32_t p = 0;
 #pragma unroll
             for (int u = 0; u < kW; ++u)
-              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= thr) p |= 1u << u;
+              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= athr) p |= 1u << u;
             ph_lo[r] = p;
             ph_hi[r] = 0u;
           } else {
@@ -354,8 +363,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
             const double d = __dsub_rn(rv, cv);
             if constexpr (M == 1) {
               setbit_le(dw[r], fabs(d), thr, 1u << t);
-            } else if constexpr (kLinfAnd) {
-              if (fabs(d) <= thr) {
+            } else if constexpr (kAnd) {
+              if (fabs(d) <= athr) {
                 if (t + kW < 32) ph_lo[r] |= 1u << ((t + kW) & 31);
                 else ph_hi[r] |= 1u << ((t + kW - 32) & 31);
               }
@@ -419,12 +428,30 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         uint32_t word;
-        if constexpr (kLinfAnd) {
+        if constexpr (kAnd) {
           word = ph_lo[r];
 #pragma unroll
           for (int k = 1; k < M; ++k) word &= __funnelshift_rc(ph_lo[r], ph_hi[r], k * TAU);
           ph_lo[r] = ph_hi[r];
           ph_hi[r] = 0u;
+          if constexpr (kPre) {  // exact sums (reference order) for the candidate cells only
+            uint32_t cand = word, res = 0u;
+            while (cand) {
+              const int t = __ffs(cand) - 1;
+              cand &= cand - 1u;
+              const double* rp = rowc + r * HS + t;
+              const double* cp = colc + t;
+              double acc = 0.0;
+#pragma unroll
+              for (int k = 0; k < M; ++k) {
+                const double d = __dsub_rn(rp[k * TAU], cp[k * TAU]);
+                const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
+                acc = (k == 0) ? term : __dadd_rn(acc, term);
+              }
+              if (acc <= thr) res |= 1u << t;
+            }
+            word = res;
+          }
         } else {
           word = dw[r];
         }
@@ -603,7 +630,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
     for (int r = R - 1; r >= 1; --r) {
       if constexpr (!kDirect && kW > 0 && !kPacked) {
-        if constexpr (kLinfAnd) {
+        if constexpr (kAnd) {
           ph_lo[r] = ph_lo[r - 1];
         } else {
 #pragma unroll

@@ -28,7 +28,7 @@ constexpr int min_blocks() {
 
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
-  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC ? 4 : 8);
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8);
   auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(), PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
@@ -39,7 +39,7 @@ cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const SymSmem L(NW, R, w, PREC ? 4 : 8);
+  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8);
   return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total,
                  &launch_unit<METRIC, M, TAU, NW, R, PREC>,
                  (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(),
@@ -59,6 +59,9 @@ bool find_variant_direct(int metric, int m, int tau, bool small, Variant* out);
 bool find_variant_f32_l1(int m, int tau, Variant* out);
 bool find_variant_f32_l2(int m, int tau, Variant* out);
 bool find_variant_f32_direct(int metric, int m, int tau, Variant* out);
+
+// Sparse prefilter kernels (PREC = 2, exact; rqa_unit.cuh kPre).
+bool find_variant_pre(int metric, int m, int tau, Variant* out);
 
 inline bool find_variant_f32(int metric, int m, int tau, bool packed_only, Variant* out) {
   if (m >= 2 && metric == kL1 && find_variant_f32_l1(m, tau, out)) return true;

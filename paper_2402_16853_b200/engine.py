@@ -45,7 +45,7 @@ def default_workers() -> int:
 
 # precision keyword -> C-ABI code (rqa_run_prec); evaluation path reported in timing
 PRECISIONS = {"fp64": 64, "fp32": 32}
-EVALUATION_PATHS = {-1: "fp64", 0: "f32-filter", 1: "fp32"}
+EVALUATION_PATHS = {-1: "fp64", 0: "f32-filter", 1: "fp32", 2: "fp64-prefilter"}
 
 
 def device_count() -> int:

@@ -104,9 +104,9 @@ def test_default_fp64_path_is_float64():
     rng = np.random.default_rng(5)
     s = rng.uniform(0, 1, 5000)
     _, timing = run_analysis(embed(s, 3, 1), AnalysisSettings(3, 1, "l2", 0.1))
-    assert timing["evaluation"] in ("fp64", "f32-filter")
+    assert timing["evaluation"] in ("fp64", "f32-filter", "fp64-prefilter")
     if "RQA_FILTER" not in os.environ:
-        assert timing["evaluation"] == "fp64"
+        assert timing["evaluation"] != "f32-filter"
 
 
 _CHILD = r"""
@@ -142,4 +142,56 @@ def test_filter_modes_in_subprocess(mode, expect):
     for kind, m, tau, metric, ok, ev in rows:
         assert ok, (kind, m, tau, metric, ev)
         want = expect or ("f32-filter" if kind == "uniform" else "fp64")
-        assert ev == want, (kind, m, tau, metric, ev)
+        if want == "fp64":
+            assert ev in ("fp64", "fp64-prefilter"), (kind, m, tau, metric, ev)
+        else:
+            assert ev == want, (kind, m, tau, metric, ev)
+
+
+_CHILD_PRE = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2402_16853_b200 import AnalysisSettings, embed, run_analysis
+from oracle.oracle import oracle_histograms
+out = []
+rng = np.random.default_rng(23)
+for kind, m, tau, metric, r, w in (("uniform", 3, 1, "l2", 0.1, 0), ("uniform", 2, 3, "l2", 0.05, 1),
+                                   ("sine", 2, 1, "l2", 0.5, 0), ("uniform", 5, 1, "l2", 0.3, 2),
+                                   ("uniform", 3, 1, "l1", 0.2, 0), ("sine", 2, 2, "l1", 1.0, 0),
+                                   ("uniform", 4, 2, "l2", 0.25, 0)):
+    n = 3100
+    s = rng.uniform(0, 1, n) if kind == "uniform" else np.sin(np.linspace(0, 60, n)) + 0.1 * rng.normal(size=n)
+    s[100] = np.nan
+    h, t = run_analysis(embed(s, m, tau), AnalysisSettings(m, tau, metric, r, theiler_corrector=w))
+    d, v, wh, p = oracle_histograms(s, m, tau, metric, r, w, tile_size=512)
+    ok = (h.recurrence_points == p and (h.diagonal == d).all() and (h.vertical == v).all()
+          and (h.white_vertical == wh).all())
+    out.append([kind, m, tau, metric, bool(ok), t["evaluation"]])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("mode,expect", [("1", "fp64-prefilter"), ("0", "fp64")])
+def test_prefilter_modes_in_subprocess(mode, expect):
+    """RQA_PREFILTER=1 forces the sparse prefilter (also on dense data), 0 disables
+    it; both must reproduce the float64 oracle bit for bit (NaN included)."""
+    env = dict(os.environ, RQA_PREFILTER=mode)
+    out = subprocess.run([sys.executable, "-c", _CHILD_PRE, REPO], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rows = json.loads(out.stdout.strip().splitlines()[-1])
+    for kind, m, tau, metric, ok, ev in rows:
+        assert ok, (kind, m, tau, metric, ev)
+        assert ev == expect, (kind, m, tau, metric, ev)
+
+
+def test_prefilter_chosen_for_sparse_c3_like(oracle_lib):
+    rng = np.random.default_rng(8)
+    s = rng.uniform(0, 1, 6000)
+    st = AnalysisSettings(3, 1, "l2", 0.1)
+    h, timing = run_analysis(embed(s, 3, 1), st)
+    if "RQA_PREFILTER" not in os.environ:
+        assert timing["evaluation"] == "fp64-prefilter"
+    want = oracle_lib.oracle_histograms(s, 3, 1, "l2", 0.1, 0, tile_size=512)
+    assert_same((h.diagonal, h.vertical, h.white_vertical, h.recurrence_points), want, "C3-like")
