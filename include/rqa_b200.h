@@ -48,11 +48,12 @@ extern "C" {
  * [0] h2d, [1] band kernel, [2] fold kernel, [3] d2h, [4] total device span,
  * [5] cells per second over the band+fold kernels, [6] band height,
  * [7] number of bands, [8] evaluation path (-1 float64 kernels, 0 f32 filter
- * with float64 re-evaluation (exact), 1 fp32 mode), [9] certified band
- * half-width of the f32 filter.  Very large n is split into row stripes
+ * with float64 re-evaluation (exact), 1 fp32 mode, 2 float64 sparse
+ * prefilter (exact)), [9] certified band half-width of the f32 filter,
+ * [10] sampled fraction of prefilter candidate cells (-1 if not sampled).  Very large n is split into row stripes
  * processed one after the other on the device when the band summaries would
  * not fit. */
-#define RQA_TIMING_SLOTS 10
+#define RQA_TIMING_SLOTS 11
 
 /* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
 int rqa_version(void);

@@ -15,7 +15,7 @@ __all__ = ["lib", "LIB_PATH", "call", "SYMBOLS", "TIMING_SLOTS"]
 
 LIB_PATH = os.environ.get("RQA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "librqa_b200.so")  # RQA_LIB_PATH: A/B testing
-TIMING_SLOTS = 10
+TIMING_SLOTS = 11
 
 _c = ctypes
 _i32, _i64, _dbl, _vp = _c.c_int32, _c.c_int64, _c.c_double, _c.c_void_p

@@ -163,6 +163,7 @@ struct Problem {
   const float* sf = nullptr;
   unsigned long long* mism = nullptr;
   double dstar = 0.0;   // prefilter bound (var.prec == 2)
+  double cand = -1.0;   // sampled prefilter candidate fraction (-1: not sampled)
 };
 
 int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
@@ -380,7 +381,8 @@ int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
     RQA_CUDA(cudaMemcpyAsync(&hits, ws->maxbits + 1, sizeof hits, cudaMemcpyDeviceToHost, st),
              "d2h");
     RQA_CUDA(cudaStreamSynchronize(st), "candidate sampling");
-    if ((double)hits / samples > kPrefilterMax) return RQA_OK;
+    p->cand = (double)hits / samples;
+    if (p->cand > kPrefilterMax) return RQA_OK;
   }
   p->dstar = dstar;
   p->var = pv;
@@ -791,6 +793,7 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
     timing[7] = (double)((p.n + p.var.band_rows() - 1) / p.var.band_rows());
     timing[8] = p.var.prec == 2 ? 2.0 : (double)p.filt;
     timing[9] = (double)p.band32;
+    timing[10] = p.cand;
   }
   return RQA_OK;
 }

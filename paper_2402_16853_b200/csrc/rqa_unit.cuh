@@ -560,24 +560,46 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         if (!(a.skip & 4) && x >= rs_[PR - 1]) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
           // shifted into aligned columns, transposed, met bottom-up
-          auto col_step = [&](int c, const int* lim) {
+          // 32-bit shared addresses of the row words (rowbuf / previous iteration)
+          const uint32_t rb_sa = smem_u32(rowbuf), pv_sa = smem_u32(prev_cur);
+          auto col_step = [&](int c, const int* lim, auto full) {
             const int wp = (wv - c) & (NW - 1);
 #pragma unroll
             for (int p = 0; p < PR; ++p) {
               const int lrow = rs_[p] * HS + 32 * c + lane;
-              const uint32_t w1 = rowbuf[wp * H + lrow];
-              const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
+              const uint32_t w1 = lds_u32(rb_sa + 4u * (uint32_t)(wp * H + lrow));
+              const uint32_t w0 = lds_u32(wp > 0 ? rb_sa + 4u * (uint32_t)((wp - 1) * H + lrow)
+                                                 : pv_sa + 4u * (uint32_t)lrow);
               const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
-              const int nb = min(max(lim[p] - 32 * c, 0), 32);
-              const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
-              runs_push(bits, nb, cur[p], 0u, evq);
+              if constexpr (decltype(full)::value) {  // every lane: 32 rows of the column
+                runs_push(__brev(colw), 32, cur[p], 0u, evq);
+              } else {
+                const int nb = min(max(lim[p] - 32 * c, 0), 32);
+                const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
+                runs_push(bits, nb, cur[p], 0u, evq);
+              }
             }
             if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
           };
+          using kFull = std::integral_constant<bool, true>;
+          using kPart = std::integral_constant<bool, false>;
+          bool fnew = true, ffin = true;
+#pragma unroll
+          for (int p = 0; p < PR; ++p) {
+            fnew &= lim_new[p] >= 32 * NCH;
+            ffin &= lim_fin[p] >= 32 * (wv + 1);
+          }
+          fnew = __all_sync(0xffffffffu, fnew);
+          ffin = __all_sync(0xffffffffu, ffin);
           // windows above the warp's own start the columns of iteration x+1
           if (do_new) {
+            if (fnew) {
 #pragma unroll 1
-            for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new);
+              for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new, kFull{});
+            } else {
+#pragma unroll 1
+              for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new, kPart{});
+            }
           }
 #pragma unroll
           for (int p = 0; p < PR; ++p) {
@@ -586,8 +608,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
           // the warp's own window and those below finish the columns of x
           if (do_fin) {
+            if (ffin) {
 #pragma unroll 1
-            for (int c = wv; c >= 0; --c) col_step(c, lim_fin);
+              for (int c = wv; c >= 0; --c) col_step(c, lim_fin, kFull{});
+            } else {
+#pragma unroll 1
+              for (int c = wv; c >= 0; --c) col_step(c, lim_fin, kPart{});
+            }
           }
 #pragma unroll
           for (int p = 0; p < PR; ++p) fin[p] = cur[p];

@@ -140,6 +140,7 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         "evaluation": EVALUATION_PATHS.get(int(tim[8]), "fp64"),
         "devices": devices,
         "f32_band": float(tim[9]),
+        "prefilter_candidates": float(tim[10]),
         "total": time.perf_counter() - started,
     }
     if precision == "fp32":
