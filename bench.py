@@ -293,7 +293,7 @@ def main():
         dev_index = torch.cuda.current_device()
         _, e2e_timing = run_analysis(emb, settings, device=dev_index)
         e2e_t = []
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(max(1, args.steps)):
             flush_l2(flush)
             torch.cuda.synchronize()
             t0 = time.perf_counter()

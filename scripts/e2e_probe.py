@@ -1,0 +1,12 @@
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2402_16853_b200 import embed, run_analysis
+from paper_2402_16853_b200.workloads import WORKLOADS
+wl = WORKLOADS["C3"]
+e = embed(wl.series(), 3, 1)
+for i in range(4):
+    t0 = time.perf_counter()
+    h, t = run_analysis(e, wl.settings, device=0)
+    w = time.perf_counter() - t0
+    print(f"wall {w*1e3:.1f} ms  h2d {t['h2d']*1e3:.1f} kern {t['create_recurrence_matrix']*1e3:.1f} fold {t['fold']*1e3:.1f} d2h {t['d2h']*1e3:.1f} dev {t['device_total']*1e3:.1f} eval {t['evaluation']}", flush=True)
