@@ -337,7 +337,20 @@ def main():
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
             traffic_src = "profiles/ncu_traffic.json (" + tr["kernel"] + ", ncu --set full)"
     except (OSError, ValueError, KeyError):
-        pass
+        tr = None
+    # issue roofline of the dominant kernel: its ncu warp-instruction count over
+    # the live kernel time vs 4 warp-instructions / clk / SM at the sampled clock
+    issue = None
+    sm_mhz = clocks.summary().get("sm_mhz")
+    if tr and world == 1 and tr.get("warp_instructions") and sm_mhz:
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ipeak = 4.0 * sms * sm_mhz * 1e6
+        t_unit = t_kern * tr["gpu_time_ms"] / (tr["gpu_time_ms"] + sum(
+            f["gpu_time_ms"] for f in tr.get("folds", {}).values()))
+        ia = tr["warp_instructions"] / t_unit
+        issue = {"unit": "warp-inst/s", "achieved": ia, "peak": ipeak, "frac": ia / ipeak,
+                 "source": "warp instructions per launch from profiles/ncu_traffic.json, "
+                           "kernel share of the timed band+fold span"}
     roofline = {
         "bound": "fp64", "unit": "FP64 op/s",
         "achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
@@ -362,6 +375,7 @@ def main():
                    "d2h_bytes_per_step": d2h},
            "gpu_launches": int(launches),
            "roofline": roofline,
+           "issue_roofline": issue,
            "clocks": clocks.summary(),
            "full_rqa_wall_s": cells / e2e_val if e2e_val else None}
     if world == 1 and not args.no_cpu_baseline:
