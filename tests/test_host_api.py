@@ -92,3 +92,19 @@ def test_ingest_spec_examples(tmp_path):
     s = generate_sine(3, math.pi)
     assert s.values[0] == 0.0 and s.values[1] == 1.0 and abs(s.values[2]) < 1e-12
     assert embed(np.arange(10.0), 2, 3).n_vectors == 7
+
+
+def test_measures_from_golden_histograms_are_bit_identical():
+    """compute_measures (sparse formulation) on the reference's own histograms
+    reproduces the reference's measures exactly (measures.py:73-139)."""
+    from fixtures import load_cases, result_arrays, settings_obj
+
+    from paper_2402_16853_b200 import LineHistograms, compute_measures
+
+    for series, st, res, meta in load_cases("small_cases"):
+        s = settings_obj(st)
+        d, v, w, p = result_arrays(res)
+        n = d.shape[0] - 1
+        got = compute_measures(LineHistograms(n, p, d, v, w), s).measures_dict()
+        for k, want in meta["measures"].items():
+            assert got[k] == want, (meta["id"], k, got[k], want)
