@@ -133,7 +133,7 @@ __host__ __device__ __forceinline__ int64_t sym_band_offset(int64_t b, int64_t n
 
 // Diagonal k >= 0 folded over the segments (height H) of [row_lo, row_hi);
 // mode as fold_kernel.  Offsets advance incrementally (compact layout).
-__global__ void sym_fold_diag(const SymFoldArgs a, const int mode) {
+__global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, const int mode) {
   const int64_t n = a.n;
   __shared__ uint32_t bins[3 * kSmemBins];
   FoldBins fb{bins};
@@ -307,7 +307,7 @@ struct UnitFoldArgs {
   uint2* out_row;              // stripe mode: row part per row (rows of the stripe)
 };
 
-__global__ void unit_fold_hooks(const UnitFoldArgs a, const int mode) {
+__global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, const int mode) {
   const int64_t n = a.n;
   __shared__ uint32_t bins[3 * kSmemBins];
   FoldBins fb{bins};
