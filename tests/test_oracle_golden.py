@@ -69,3 +69,29 @@ def test_oracle_matrix_symmetric_and_brute_force(oracle_lib):
             brute = np.array([[distance(vec[i], vec[j], metric) <= r for j in range(n)]
                               for i in range(n)])
             assert np.array_equal(mat, brute)
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2", "linf"])
+def test_oracle_fp32_mode_matches_numpy_float32(metric, oracle_lib):
+    """The fp32-mode restatement (recurrence_tile32) is numpy's float32
+    evaluation of embedding.py:137-156: samples, ufuncs and radius in float32."""
+    rng = np.random.default_rng(11)
+    for m, tau, kind in ((1, 1, "u"), (3, 2, "u"), (4, 1, "o"), (2, 3, "o")):
+        s = rng.uniform(0, 1, 300) if kind == "u" else 100 + rng.uniform(0, 1e-3, 300)
+        r = 0.3 if kind == "u" else 3e-4
+        n = len(s) - (m - 1) * tau
+        s32 = s.astype(np.float32)
+        acc = None
+        for k in range(m):
+            d = s32[k * tau:k * tau + n][:, None] - s32[k * tau:k * tau + n][None, :]
+            t = d * d if (metric == "l2" and m > 1) else np.abs(d)
+            acc = t if k == 0 else (np.maximum(acc, t) if metric == "linf" else acc + t)
+        if metric == "l2" and m > 1:
+            acc = np.sqrt(acc)
+        want = acc <= np.float32(r)
+        got = oracle_lib.oracle_matrix(s, m, tau, metric, r, 0, precision=32)
+        assert np.array_equal(got, want), (metric, m, tau, kind)
+        d, v, w, p, mism = oracle_lib.oracle_histograms_prec(s, m, tau, metric, r, 0,
+                                                             precision=32, tile_size=64)
+        m64 = oracle_lib.oracle_matrix(s, m, tau, metric, r, 0)
+        assert p == int(want.sum()) and mism == int((m64 != want).sum())
