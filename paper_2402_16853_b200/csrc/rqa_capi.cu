@@ -408,8 +408,12 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
     X[b] = (nrem + D - 1) / D + R - 1;
     total += X[b];
   }
-  // aim for >= 4 waves of units; one recomputed iteration per unit boundary
-  int64_t len = std::max<int64_t>(8, total / std::max<int64_t>(1, 4LL * slots));
+  // aim for >= 16 waves of units (RQA_WAVES overrides; 4 waves left a 5-8 %
+  // tail, measured with scripts/stripe_projection.py); one recomputed
+  // iteration per unit boundary
+  static const char* wenv = getenv("RQA_WAVES");
+  const int64_t waves = wenv ? std::max(1, atoi(wenv)) : 16;
+  int64_t len = std::max<int64_t>(8, total / std::max<int64_t>(1, waves * slots));
   UnitPlan pl;
   pl.band_start.assign(nb + 1, 0);
   for (int64_t b = 0; b < nb; ++b) {
