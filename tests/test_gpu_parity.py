@@ -214,3 +214,27 @@ def test_full_size_identities():
         rr_full = p / (n * n)
         rr_pref = fx["result"]["recurrence_points"] / 65536 ** 2
         assert abs(rr_full - rr_pref) < 2e-4
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 257, 1023, 1025])
+def test_tiny_and_boundary_sizes(n, oracle_lib):
+    """n around warp / slot / band boundaries, every metric, both kernel families."""
+    rng = np.random.default_rng(n)
+    for metric, m, tau, r in (("l2", 3, 1, 0.3), ("l1", 2, 2, 0.2), ("linf", 1, 1, 0.1),
+                              ("l2", 6, 2, 0.6)):
+        s = rng.uniform(0, 1, n + (m - 1) * tau)
+        for w in (0, 1, 3):
+            st = AnalysisSettings(m, tau, metric, r, theiler_corrector=w)
+            want = oracle_lib.oracle_histograms(s, m, tau, metric, r, w, tile_size=64)
+            assert_same(gpu_hist(s, st), want, f"n={n} {metric} m{m} t{tau} w{w}")
+
+
+def test_largest_embedding_window(oracle_lib):
+    """(m - 1) * tau = 4096 (the direct kernel's largest window)."""
+    rng = np.random.default_rng(4)
+    for m, tau in ((2, 4096), (4097, 1)):
+        s = rng.uniform(0, 1, 4096 + 300)
+        r = 0.5 if m == 2 else 30.0
+        st = AnalysisSettings(m, tau, "l1", r)
+        want = oracle_lib.oracle_histograms(s, m, tau, "l1", r, 0, tile_size=128)
+        assert_same(gpu_hist(s, st), want, f"m{m} t{tau}")
