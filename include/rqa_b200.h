@@ -55,6 +55,9 @@ extern "C" {
  * not fit. */
 #define RQA_TIMING_SLOTS 11
 
+/* rqa_run_prec flags */
+#define RQA_FLAG_OUT_ZEROED 1
+
 /* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
 int rqa_version(void);
 
@@ -94,10 +97,12 @@ int rqa_run(const double *series, int64_t len, int32_t m, int32_t tau, int32_t m
  *       float32 semantics); *mismatches (may be NULL) receives the number of
  *       cells of the full n x n matrix whose fp32 decision differs from the
  *       float64 one.
+ * flags: RQA_FLAG_OUT_ZEROED -- diag/vert/white are already zero-filled; only
+ *       the nonzero bins are copied back (compacted on the device).
  */
 int rqa_run_prec(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                  double radius, int64_t theiler, int32_t precision, int32_t device,
-                 int64_t *diag, int64_t *vert, int64_t *white, int64_t *points,
+                 int32_t flags, int64_t *diag, int64_t *vert, int64_t *white, int64_t *points,
                  int64_t *mismatches, double *timing, char *err, size_t errlen);
 
 /*

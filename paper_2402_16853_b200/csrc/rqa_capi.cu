@@ -118,6 +118,8 @@ struct Workspace {
   size_t bounds_cap = 0;
   int32_t* gather = nullptr;   // multi-device: gathered stripe summaries (device 0 only)
   size_t gather_cap = 0;
+  unsigned long long* bins = nullptr;  // sparse D2H: [1 counter word][2 * kSparseCap pairs]
+  size_t bins_cap = 0;
   cudaEvent_t ev[6] = {};
   bool init = false;
 };
@@ -256,6 +258,23 @@ __global__ void sample_candidates_kernel(const double* __restrict__ s, int64_t n
   for (int k = 0; k < m && c; ++k)
     c = fabs(__dsub_rn(s[i + (int64_t)k * tau], s[j + (int64_t)k * tau])) <= dstar;
   if (c) atomicAdd(hits, 1ull);
+}
+
+// Nonzero histogram bins as (index, count) pairs (sparse D2H of the results).
+__global__ void compact_bins_kernel(const unsigned long long* __restrict__ h, int64_t count,
+                                    unsigned long long* __restrict__ out, unsigned int* counter,
+                                    unsigned int cap) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = h[q];
+    if (v) {
+      const unsigned int slot = atomicAdd(counter, 1u);
+      if (slot < cap) {
+        out[2 * (size_t)slot] = (unsigned long long)q;
+        out[2 * (size_t)slot + 1] = v;
+      }
+    }
+  }
 }
 
 __global__ void prep_f32_kernel(const double* __restrict__ s, float* __restrict__ sf, int64_t count,
@@ -735,7 +754,7 @@ int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t* ba
 
 int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                  double radius, int64_t theiler, int32_t precision, int32_t device,
-                 int64_t* diag, int64_t* vert, int64_t* white, int64_t* points,
+                 int32_t flags, int64_t* diag, int64_t* vert, int64_t* white, int64_t* points,
                  int64_t* mismatches, double* timing, char* err, size_t errlen) {
   if (!series || !diag || !vert || !white || !points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
@@ -772,9 +791,44 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
   rc = run_full(ws, p, ws->hist, ws->hist + 3 * hn, st, ws->ev[2], err, errlen);
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[3], st), "event");
-  RQA_CUDA(cudaMemcpyAsync(diag, ws->hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
-  RQA_CUDA(cudaMemcpyAsync(vert, ws->hist + hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
-  RQA_CUDA(cudaMemcpyAsync(white, ws->hist + 2 * hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  // outputs: the nonzero bins only when the caller's arrays are zero-filled
+  // (RQA_FLAG_OUT_ZEROED) and they fit the pair buffer, else dense copies
+  bool dense = true;
+  if (flags & RQA_FLAG_OUT_ZEROED) {
+    constexpr unsigned int kSparseCap = 1u << 20;
+    RQA_CUDA(grow(&ws->bins, &ws->bins_cap, 1 + 2 * (size_t)kSparseCap), "allocating bins");
+    unsigned int* counter = reinterpret_cast<unsigned int*>(ws->bins);
+    RQA_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st), "memset");
+    const int64_t nb3 = 3 * (int64_t)hn;
+    compact_bins_kernel<<<(int)std::min<int64_t>((nb3 + 255) / 256, 148 * 8), 256, 0, st>>>(
+        ws->hist, nb3, ws->bins + 1, counter, kSparseCap);
+    RQA_CUDA(cudaGetLastError(), "launching bin compaction");
+    g_launches++;
+    unsigned long long cnt = 0;
+    RQA_CUDA(cudaMemcpyAsync(&cnt, ws->bins, sizeof cnt, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaStreamSynchronize(st), "bin compaction");
+    cnt &= 0xffffffffull;
+    if (cnt <= kSparseCap) {
+      std::vector<unsigned long long> pairs(2 * cnt + 2);
+      if (cnt)
+        RQA_CUDA(cudaMemcpyAsync(pairs.data(), ws->bins + 1, 2 * cnt * 8, cudaMemcpyDeviceToHost,
+                                 st),
+                 "d2h");
+      RQA_CUDA(cudaStreamSynchronize(st), "d2h");
+      int64_t* outs[3] = {diag, vert, white};
+      for (unsigned long long q = 0; q < cnt; ++q) {
+        const uint64_t idx = pairs[2 * q];
+        outs[idx / hn][idx % hn] = (int64_t)pairs[2 * q + 1];
+      }
+      dense = false;
+    }
+  }
+  if (dense) {
+    RQA_CUDA(cudaMemcpyAsync(diag, ws->hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaMemcpyAsync(vert, ws->hist + hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaMemcpyAsync(white, ws->hist + 2 * hn, hn * 8, cudaMemcpyDeviceToHost, st),
+             "d2h");
+  }
   RQA_CUDA(cudaMemcpyAsync(points, ws->hist + 3 * hn, 8, cudaMemcpyDeviceToHost, st), "d2h");
   if (mismatches)
     RQA_CUDA(cudaMemcpyAsync(mismatches, ws->hist + 3 * hn + 1, 8, cudaMemcpyDeviceToHost, st),
@@ -824,8 +878,8 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
       return set_err(err, errlen, "device %d out of range (%d visible)", devices[g], ndev),
              RQA_EINVAL;
   if (n_devices == 1)
-    return rqa_run_prec(series, len, m, tau, metric, radius, theiler, precision, devices[0], diag,
-                        vert, white, points, mismatches, timing, err, errlen);
+    return rqa_run_prec(series, len, m, tau, metric, radius, theiler, precision, devices[0], 0,
+                        diag, vert, white, points, mismatches, timing, err, errlen);
   const auto t0 = std::chrono::steady_clock::now();
   const int G = n_devices;
   const std::vector<int64_t> bounds = area_stripes(p.n, G, 1024);
@@ -917,8 +971,8 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
 int rqa_run(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
             double radius, int64_t theiler, int32_t device, int64_t* diag, int64_t* vert,
             int64_t* white, int64_t* points, double* timing, char* err, size_t errlen) {
-  return rqa_run_prec(series, len, m, tau, metric, radius, theiler, 64, device, diag, vert, white,
-                      points, nullptr, timing, err, errlen);
+  return rqa_run_prec(series, len, m, tau, metric, radius, theiler, 64, device, 0, diag, vert,
+                      white, points, nullptr, timing, err, errlen);
 }
 
 int rqa_run_device_prec(const double* d_series, int64_t len, int32_t m, int32_t tau,
@@ -1046,6 +1100,7 @@ int rqa_release(void) {
     if (!ws) continue;
     cudaSetDevice((int)(d % kMaxDevices));
     cudaFree(ws->gather);
+    cudaFree(ws->bins);
     cudaFree(ws->s_pad);
     cudaFree(ws->sf_pad);
     cudaFree(ws->maxbits);

@@ -45,6 +45,7 @@ def default_workers() -> int:
 
 # precision keyword -> C-ABI code (rqa_run_prec); evaluation path reported in timing
 PRECISIONS = {"fp64": 64, "fp32": 32}
+FLAG_OUT_ZEROED = 1  # rqa_run_prec flags (include/rqa_b200.h)
 EVALUATION_PATHS = {-1: "fp64", 0: "f32-filter", 1: "fp32", 2: "fp64-prefilter"}
 
 
@@ -120,8 +121,8 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     outs = (diag.ctypes.data_as(p64), vert.ctypes.data_as(p64), white.ctypes.data_as(p64),
             pts.ctypes.data_as(p64), mism.ctypes.data_as(p64),
             tim.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-    if len(devices) == 1:
-        _native.call("rqa_run_prec", *args, devices[0], *outs)
+    if len(devices) == 1:  # outputs are fresh np.zeros: only nonzero bins come back
+        _native.call("rqa_run_prec", *args, devices[0], FLAG_OUT_ZEROED, *outs)
     else:
         dv = (ctypes.c_int32 * len(devices))(*devices)
         _native.call("rqa_run_multi", *args, dv, len(devices), *outs)
