@@ -310,6 +310,12 @@ def main():
             analyze(series_np, settings, device=dev_index)
             e2e_t.append(time.perf_counter() - t0)
         e2e_val = cells / float(np.mean(e2e_t))
+        # results come back as device-compacted nonzero bins (16 B each) plus
+        # the counter and the point count (run_analysis, RQA_FLAG_OUT_ZEROED)
+        res_h = analyze(series_np, settings, device=dev_index).histograms
+        nnz = sum(int(np.count_nonzero(a)) for a in (res_h.diagonal, res_h.vertical,
+                                                     res_h.white_vertical))
+        d2h = 16 * nnz + 8 + 8
         full_rqa = {"median_s": float(np.median(e2e_t)), "min_s": float(np.min(e2e_t)),
                     "max_s": float(np.max(e2e_t)), "runs": len(e2e_t), "init_s": init_s,
                     "api": "paper_2402_16853_b200.analyze (embed -> run_analysis -> "

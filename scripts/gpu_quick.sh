@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/q_all.log 2>&1; tail -2 gpurun_out/q_all.log
-timeout 300 python scripts/e2e_probe.py 2>&1 | tail -3
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2> gpurun_out/b.err; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print(d['value'], d['e2e']['value'], d['full_rqa'])"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"fold" python scripts/profile_once.py C3 2 > gpurun_out/fold_t.csv 2>&1
+grep fold gpurun_out/fold_t.csv | python3 -c "
+import csv,sys
+for r in csv.reader(sys.stdin): print(r[4][:20], r[-1])"
