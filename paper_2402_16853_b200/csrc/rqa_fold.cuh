@@ -11,78 +11,11 @@
 #pragma once
 #include "rqa_device.cuh"
 
-namespace rqa {
-
-enum FoldMode : int { kFoldFinal = 0, kFoldStripe = 1 };
-
-template <typename TS>
-struct FoldArgs {
-  const TS* P;              // [nseg][pitch]
-  const TS* S;              // [nseg][pitch]
-  int64_t pitch;
-  const int64_t* bounds;    // nseg+1 row boundaries (device)
-  int nseg;
-  int64_t n;
-  unsigned long long* hist; // [3][n+1] (only the diagonal part is touched)
-  int32_t* out_p;           // stripe mode: prefix of the whole stripe per k
-  int32_t* out_s;           // stripe mode: suffix of the whole stripe per k
-};
-
-template <typename TS>
-__global__ void fold_kernel(const FoldArgs<TS> a, const int mode) {
-  const int64_t n = a.n;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long wgt = (k == 0) ? 1ull : 2ull;
-    const int64_t rows = n - k;  // diagonal k has rows [0, n-k)
-    int64_t open = 0;
-    int64_t pstr = -1;
-    for (int g = 0; g < a.nseg; ++g) {
-      const int64_t lo = a.bounds[g], hi = a.bounds[g + 1];
-      if (lo >= rows) break;
-      const int64_t L = min(hi, rows) - lo;
-      const int64_t p = (int64_t)a.P[g * a.pitch + k];
-      if (p == L) {  // the whole segment is one run: keep it open
-        open += L;
-        continue;
-      }
-      const int64_t x = open + p;
-      if (mode == kFoldStripe && pstr < 0) {
-        pstr = x;
-      } else if (x > 0) {
-        atomicAdd(&a.hist[kDiag * (n + 1) + x], wgt);
-      }
-      open = (hi <= rows) ? (int64_t)a.S[g * a.pitch + k] : 0;
-    }
-    if (mode == kFoldFinal) {
-      if (open > 0) atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
-    } else {
-      const int64_t top = a.bounds[0], bot = a.bounds[a.nseg];
-      int64_t sstr = 0;
-      if (top >= rows) {
-        pstr = 0;                 // diagonal does not reach this stripe
-      } else if (pstr < 0) {
-        pstr = open;              // stripe is one run (full)
-        sstr = open;
-      } else if (bot <= rows) {
-        sstr = open;              // run open at the stripe's bottom edge
-      } else if (open > 0) {      // diagonal ended inside the stripe
-        atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
-      }
-      a.out_p[k] = (int32_t)pstr;
-      a.out_s[k] = (int32_t)sstr;
-    }
-  }
-}
-
-}  // namespace rqa
-
-// ===========================================================================
-// Folds of the upper-triangle kernel (rqa_sym.cuh).
-// ===========================================================================
 #include "rqa_runs.cuh"
 
 namespace rqa {
+
+enum FoldMode : int { kFoldFinal = 0, kFoldStripe = 1 };
 
 struct SymFoldArgs {
   // band level (compact layout, see band_offset)
@@ -132,7 +65,8 @@ __host__ __device__ __forceinline__ int64_t sym_band_offset(int64_t b, int64_t n
 }
 
 // Diagonal k >= 0 folded over the segments (height H) of [row_lo, row_hi);
-// mode as fold_kernel.  Offsets advance incrementally (compact layout).
+// mode: kFoldFinal counts every run, kFoldStripe reports the runs touching
+// the stripe's top / bottom edges.  Offsets advance incrementally (compact layout).
 __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, const int mode) {
   const int64_t n = a.n;
   __shared__ uint32_t bins[3 * kSmemBins];
@@ -196,93 +130,6 @@ __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, con
     }
   }
   fb.flush(a.hist, n);
-}
-
-__device__ __forceinline__ void hook_finish(Seg acc, uint32_t lead, const GHist& h) {
-  if (acc.first == 0u) {
-    emit_run(lead, h);
-    return;
-  }
-  if (run_bit(acc.last) == run_bit(lead)) {
-    const uint32_t m = run_pack(run_len(acc.last) + run_len(lead), run_bit(lead));
-    if (!acc.uniform) emit_run(acc.first, h);
-    emit_run(m, h);
-  } else {
-    emit_run(acc.first, h);
-    if (!acc.uniform) emit_run(acc.last, h);
-    emit_run(lead, h);
-  }
-}
-
-// Hook c (= column c of the full matrix): column-part segments of the bands
-// of [row_lo, row_hi) above row c, then (final mode) the row part's lead.
-__global__ void sym_fold_hooks(const SymFoldArgs a, const int mode) {
-  const int64_t n = a.n;
-  const GHist h{a.hist, n + 1};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    Seg acc{0u, 0u, 0u};
-    for (int g = 0; g < a.nb; ++g) {
-      const int64_t lo = a.row_lo + g * a.H;
-      if (lo >= c) break;
-      const int64_t hi = min(lo + a.H, a.row_hi);
-      const int64_t L = min(hi, c) - lo;
-      const uint32_t v = a.colsum[sym_band_offset(g, n, a.row_lo, a.H) + (c - lo)];
-      const uint32_t top = v >> 16, bot = v & 0xffffu;
-      const Seg s{top, bot, (int64_t)run_len(top) == L ? 1u : 0u};
-      acc = seg_combine(acc, s, h);
-    }
-    if (mode == kFoldFinal) {
-      hook_finish(acc, a.rowlead[c], h);
-    } else {
-      a.out_col[c] = make_uint2(acc.first, acc.last);
-    }
-  }
-}
-
-// Final fold over stripes (multi-GPU): diagonals and hooks.
-__global__ void sym_fold_stripes(const SymFoldArgs a) {
-  const int64_t n = a.n;
-  const GHist h{a.hist, n + 1};
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    // diagonal k
-    {
-      const unsigned long long wgt = (k == 0) ? 1ull : 2ull;
-      const int64_t rows = n - k;
-      int64_t open = 0;
-      for (int g = 0; g < a.nseg; ++g) {
-        const int64_t lo = a.bounds[g], hi = a.bounds[g + 1];
-        if (lo >= rows) break;
-        if (hi <= lo) continue;
-        const int64_t L = min(hi, rows) - lo;
-        const int64_t p = a.sp[g * n + k];
-        if (p == L) {
-          open += L;
-          continue;
-        }
-        const int64_t x = open + p;
-        if (x > 0) atomicAdd(&a.hist[kDiag * (n + 1) + x], wgt);
-        open = (hi <= rows) ? (int64_t)a.ss[g * n + k] : 0;
-      }
-      if (open > 0) atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
-    }
-    // hook c = k
-    {
-      const int64_t c = k;
-      Seg acc{0u, 0u, 0u};
-      for (int g = 0; g < a.nseg; ++g) {
-        const int64_t lo = a.bounds[g], hi = a.bounds[g + 1];
-        if (lo >= c) break;
-        if (hi <= lo) continue;
-        const int64_t L = min(hi, c) - lo;
-        const uint2 v = a.scol[g * n + c];
-        const Seg s{v.x, v.y, (int64_t)run_len(v.x) == L ? 1u : 0u};
-        acc = seg_combine(acc, s, h);
-      }
-      hook_finish(acc, a.rowlead[c], h);
-    }
-  }
 }
 
 }  // namespace rqa

@@ -1,7 +1,7 @@
 // rqa_unit.cuh -- upper-triangle kernel over 2-D work units.
 //
 // A work unit is (band b, iteration range [x_a, x_b)) of the diagonal sweep
-// of sym_kernel (rqa_sym.cuh): bands of H = R*HS rows are cut along the sweep
+// of the upper-triangle band kernel: bands of H = R*HS rows are cut along the sweep
 // so that every CTA gets a bounded amount of work, which balances the SMs
 // for any n and lets a GPU's share of a multi-GPU run be spread over all of
 // its SMs.  What crosses a unit boundary is stitched by the folds:
@@ -14,7 +14,8 @@
 //     x; a unit recomputes iteration x_a-1 (cells and row words only) to own
 //     the lower parts of the columns it finishes, and leaves the columns that
 //     finish at x_b to the next unit.
-// Arithmetic, bit conventions and run extraction are those of sym_kernel.
+// Lane delta of warp v walks diagonal kd = x*D - r*HS + 32v + lane of slot r;
+// the four slots of a lane share the column of every step.
 #pragma once
 #include <type_traits>
 

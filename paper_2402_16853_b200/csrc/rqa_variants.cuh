@@ -2,7 +2,6 @@
 #pragma once
 #include <cstdlib>
 
-#include "rqa_pipe.cuh"
 #include "rqa_sym.cuh"
 #include "rqa_unit.cuh"
 

@@ -115,7 +115,7 @@ def _combine(a, b, hist):
 
 
 def stitch(pre, suf, col, lead, bounds, n, hist):
-    """Final fold over stripes (rqa_fold.cuh sym_fold_stripes)."""
+    """Final fold over stripes (rqa_fold.cuh unit_fold_stripes)."""
     for k in range(n):
         rows = n - k
         w = 1 if k == 0 else 2
