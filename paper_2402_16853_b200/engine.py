@@ -46,6 +46,9 @@ def default_workers() -> int:
 # precision keyword -> C-ABI code (rqa_run_prec); evaluation path reported in timing
 PRECISIONS = {"fp64": 64, "fp32": 32}
 FLAG_OUT_ZEROED = 1  # rqa_run_prec flags (include/rqa_b200.h)
+# below this many vectors the default device list is one GPU: a stripe would be
+# smaller than a few waves of work units and the gather/stitch would dominate
+MULTI_DEVICE_MIN_VECTORS = 1 << 16
 EVALUATION_PATHS = {-1: "fp64", 0: "f32-filter", 1: "fp32", 2: "fp64-prefilter"}
 
 
@@ -100,7 +103,12 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
             or embedded.time_delay != settings.time_delay):
         raise InvalidArgument("embedded series and settings disagree on m / tau")
     if devices is None:
-        devices = [device] if device is not None else list(range(max(1, device_count())))
+        if device is not None:
+            devices = [device]
+        else:  # every visible GPU, except for matrices too small to split usefully
+            devices = list(range(max(1, device_count())))
+            if embedded.n_vectors < MULTI_DEVICE_MIN_VECTORS:
+                devices = devices[:1]
     devices = [int(d) for d in devices]
     if not devices:
         raise InvalidArgument("devices must not be empty")
