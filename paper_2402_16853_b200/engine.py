@@ -78,8 +78,9 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     tile_size / workers do not change the results (as in the reference).
     ``devices``: CUDA device ids to split the rows over (one host thread per
     device, stripes stitched on the first; a device may repeat); default: the
-    single ``device`` if given, else every visible GPU.  Results do not
-    depend on the device list.
+    single ``device`` if given, else every visible GPU (one GPU below
+    MULTI_DEVICE_MIN_VECTORS vectors).  Results do not depend on the device
+    list.
     ``precision``: "fp64" (default) is bit-exact against the float64
     reference; "fp32" evaluates with float32 samples, arithmetic and radius
     and reports ``timing["mismatched_cells"]``, the number of cells of the
