@@ -372,11 +372,14 @@ int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
 }
 
 // Sparse prefilter plan (precision 64, float64 kernels): sample the fraction
-// of cells whose m components all lie within D*; below kPrefilterMax the
+// of cells whose m components all lie within D*; below prefilter_max(m) the
 // prefilter kernel (AND of predicates + exact sums of the candidates) issues
 // fewer instructions than the term-window kernel.  RQA_PREFILTER=0 disables,
 // =1 forces it whenever a variant exists.  Results are identical either way.
-constexpr double kPrefilterMax = 0.05;
+// The exact term-reuse kernel costs about m + 2 FP64 ops per cell, the
+// prefilter 2 plus the candidates' full sums, so its break-even candidate
+// fraction grows with m.
+inline double prefilter_max(int m) { return 0.05 * std::max(1.0, m / 3.0); }
 
 int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
   if (p->precision != 64 || p->filt != -1) return RQA_OK;
@@ -401,7 +404,7 @@ int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
              "d2h");
     RQA_CUDA(cudaStreamSynchronize(st), "candidate sampling");
     p->cand = (double)hits / samples;
-    if (p->cand > kPrefilterMax) return RQA_OK;
+    if (p->cand > prefilter_max(p->m)) return RQA_OK;
   }
   p->dstar = dstar;
   p->var = pv;

@@ -60,14 +60,20 @@ __host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot
   return ((top & 0xffffu) << 16) | (bot & 0xffffu);
 }
 
+// Candidate cells one warp resolves cooperatively per batch of two slots of a
+// 32-step chunk (sparse prefilter with large windows); more fall back to
+// per-lane resolution.  256 keeps two CTAs per SM.
+constexpr int kCandCap = 256;
+
 struct SymSmem {
   int H, HS, D, W, CW;
   size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_rowst, off_queue,
-      off_hist, total;
+      off_hist, off_cand, off_cres, total;
   // esize 8: float64 row/column windows; 4: float32 windows (f32 filter
   // kernels), the row window stored as R/2 interleaved slot pairs of
   // HS + W + 4 float2 each (rqa_unit.cuh, packed f32x2 evaluation).
-  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8) {
+  // coop: per-warp candidate list + result words (prefilter, large windows)
+  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, bool coop = false) {
     D = 32 * NW;
     HS = D;
     H = R * HS;
@@ -89,7 +95,9 @@ struct SymSmem {
     off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
     off_queue = off_rowst + (size_t)R * D * sizeof(uint2);
     off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
-    total = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;
+    off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;  // after the mbarriers
+    off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
+    total = off_cres + (coop ? (size_t)NW * R * 32 * sizeof(uint32_t) : 0);
   }
 };
 

@@ -105,6 +105,12 @@ __device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int
   return make_uint2(w64, w32);
 }
 
+// Prefilter candidates are resolved warp-cooperatively (32 at a time from a
+// shared list) when a candidate's exact sum is long (m >= 5); for short sums
+// the per-lane loop is cheaper than building the list.
+template <int PREC, int M>
+constexpr bool kCoopResolve = (PREC == 2) && (M >= 5);
+
 template <int METRIC, int M, int TAU, int NW, int R, int MINB, int PREC = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
 unit_kernel(const UnitArgs ua, const int W_rt) {
@@ -124,7 +130,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   constexpr bool kAnd = kLinfAnd || kPre;
   constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
   constexpr int NCH = HS / 32;  // == NW
-  static_assert(kAnd ? kW <= 32 : kW <= 48, "term window too large");
+  static_assert(kAnd ? kW <= 96 : kW <= 48, "term window too large");
+  // predicate window of the AND kernels: 32 steps + kW look-ahead bits
+  constexpr int NPH = 1 + (kW + 31) / 32;
   static_assert(PREC != 2 || kPre, "prefilter: L1/L2 term-reuse kernels only");
   constexpr bool kF32 = (PREC == 1);
   // packed f32x2 evaluation over slot pairs (2r, 2r+1): L1/L2 term reuse
@@ -133,7 +141,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   using F = typename std::conditional<kF32, float, double>::type;
   constexpr int RP = (R + 1) / 2;  // slot pairs
   const int W = kDirect ? W_rt : kW;
-  const SymSmem L(NW, R, W, (int)sizeof(F));
+  const SymSmem L(NW, R, W, (int)sizeof(F), kCoopResolve<PREC, M>);
   const int PS = HS + W + 4;       // packed row window: float2 elements per slot pair
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -160,6 +168,17 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   const int theiler = (int)min(a.theiler, (int64_t)1 << 30);
   const double thr = a.thr;
   const double athr = kPre ? a.dstar : thr;  // per-component predicate threshold
+  // exact float64 sum of one prefilter candidate, in the reference's order
+  auto pre_exact = [&](const F* rp, const F* cp) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < (M > 0 ? M : 1); ++k) {
+      const double d = __dsub_rn((double)rp[k * TAU], (double)cp[k * TAU]);
+      const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
+      acc = (k == 0) ? term : __dadd_rn(acc, term);
+    }
+    return acc <= thr;
+  };
   const int xa = unit.xa, xb = unit.xb;
   const int xfirst = xa > 0 ? xa - 1 : 0;  // xa-1: recomputed for the columns finishing at xa
   const int64_t goff0 = b * R;              // global slot index of slot 0
@@ -211,12 +230,12 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   double win[R][kW > 0 ? kW : 1];
   unsigned long long win2[RP][kW > 0 ? kW : 1];  // packed f32 term windows (kPacked)
   unsigned long long mism = 0;                   // fp32 mode: mismatched cells
-  uint32_t ph_lo[R], ph_hi[R];
+  uint32_t ph[R][NPH];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     st[r] = RunState{0u, 0u};
-    ph_lo[r] = 0u;
-    ph_hi[r] = 0u;
+#pragma unroll
+    for (int q = 0; q < NPH; ++q) ph[r][q] = 0u;
   }
   uint32_t pts = 0;
   unsigned long long pts64 = 0;
@@ -262,12 +281,12 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       if (r == 0 || x == xfirst) {
         if constexpr (!kDirect && kW > 0 && !kPacked) {
           if constexpr (kAnd) {
-            uint32_t p = 0;
+#pragma unroll
+            for (int q = 0; q < NPH; ++q) ph[r][q] = 0u;
 #pragma unroll
             for (int u = 0; u < kW; ++u)
-              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= athr) p |= 1u << u;
-            ph_lo[r] = p;
-            ph_hi[r] = 0u;
+              if (fabs(__dsub_rn(s_row[r * HS + u], s_col[u])) <= athr)
+                ph[r][u >> 5] |= 1u << (u & 31);
           } else {
 #pragma unroll
             for (int u = 0; u < kW; ++u) {
@@ -366,8 +385,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               setbit_le(dw[r], fabs(d), thr, 1u << t);
             } else if constexpr (kAnd) {
               if (fabs(d) <= athr) {
-                if (t + kW < 32) ph_lo[r] |= 1u << ((t + kW) & 31);
-                else ph_hi[r] |= 1u << ((t + kW - 32) & 31);
+                ph[r][(t + kW) >> 5] |= 1u << ((t + kW) & 31);
               }
             } else {
               const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
@@ -426,30 +444,95 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
         }
       }
+      if constexpr (kCoopResolve<PREC, M>) {
+        // candidate words of every slot, then the exact sums 32 candidates at
+        // a time from a per-warp list (full SIMD width), results ORed back
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t w = ph[r][0];
+#pragma unroll
+          for (int k = 1; k < M; ++k)
+            w &= __funnelshift_rc(ph[r][(k * TAU) >> 5], ph[r][((k * TAU) >> 5) + 1],
+                                  (k * TAU) & 31);
+#pragma unroll
+          for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
+          ph[r][NPH - 1] = 0u;
+          dw[r] = w;
+        }
+        constexpr int RB = (R >= 2) ? 2 : 1;  // slots per cooperative batch
+        uint16_t* cl = reinterpret_cast<uint16_t*>(smem + L.off_cand) + wv * kCandCap;
+        uint32_t* cres = reinterpret_cast<uint32_t*>(smem + L.off_cres) + wv * R * 32;
+#pragma unroll
+        for (int r0 = 0; r0 < R; r0 += RB) {
+          int kc = 0;
+#pragma unroll
+          for (int r = r0; r < r0 + RB; ++r) kc += __popc(dw[r]);
+          const int K = (int)__reduce_add_sync(0xffffffffu, (unsigned)kc);
+          if (K > 0 && K <= kCandCap) {
+            int incl = kc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            int pos = incl - kc;
+#pragma unroll
+            for (int r = r0; r < r0 + RB; ++r) {
+              uint32_t w = dw[r];
+              while (w) {
+                const int t = __ffs(w) - 1;
+                w &= w - 1u;
+                cl[pos++] = (uint16_t)((r << 10) | (lane << 5) | t);
+              }
+              cres[r * 32 + lane] = 0u;
+            }
+            __syncwarp();
+            for (int base = 0; base < K; base += 32) {
+              const int idx = base + lane;
+              if (idx < K) {
+                const uint32_t e = cl[idx];
+                const int r = (int)(e >> 10), sl = (int)((e >> 5) & 31u), t = (int)(e & 31u);
+                if (pre_exact(rowc + r * HS + t, colc - lane + sl + t))
+                  atomicOr(&cres[r * 32 + sl], 1u << t);
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = r0; r < r0 + RB; ++r) dw[r] = cres[r * 32 + lane];
+            __syncwarp();
+          } else if (K > 0) {  // very dense: every lane resolves its own cells
+#pragma unroll
+            for (int r = r0; r < r0 + RB; ++r) {
+              uint32_t cand = dw[r], res = 0u;
+              while (cand) {
+                const int t = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                if (pre_exact(rowc + r * HS + t, colc + t)) res |= 1u << t;
+              }
+              dw[r] = res;
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         uint32_t word;
-        if constexpr (kAnd) {
-          word = ph_lo[r];
+        if constexpr (kAnd && !kCoopResolve<PREC, M>) {
+          word = ph[r][0];
 #pragma unroll
-          for (int k = 1; k < M; ++k) word &= __funnelshift_rc(ph_lo[r], ph_hi[r], k * TAU);
-          ph_lo[r] = ph_hi[r];
-          ph_hi[r] = 0u;
-          if constexpr (kPre) {  // exact sums (reference order) for the candidate cells only
+          for (int k = 1; k < M; ++k)
+            word &= __funnelshift_rc(ph[r][(k * TAU) >> 5], ph[r][((k * TAU) >> 5) + 1],
+                                     (k * TAU) & 31);
+#pragma unroll
+          for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
+          ph[r][NPH - 1] = 0u;
+          if constexpr (kPre && !kCoopResolve<PREC, M>) {
+            // exact sums (reference order) for the candidate cells only
             uint32_t cand = word, res = 0u;
             while (cand) {
               const int t = __ffs(cand) - 1;
               cand &= cand - 1u;
-              const double* rp = rowc + r * HS + t;
-              const double* cp = colc + t;
-              double acc = 0.0;
-#pragma unroll
-              for (int k = 0; k < M; ++k) {
-                const double d = __dsub_rn(rp[k * TAU], cp[k * TAU]);
-                const double term = kSquare ? __dmul_rn(d, d) : fabs(d);
-                acc = (k == 0) ? term : __dadd_rn(acc, term);
-              }
-              if (acc <= thr) res |= 1u << t;
+              if (pre_exact(rowc + r * HS + t, colc + t)) res |= 1u << t;
             }
             word = res;
           }
@@ -659,7 +742,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     for (int r = R - 1; r >= 1; --r) {
       if constexpr (!kDirect && kW > 0 && !kPacked) {
         if constexpr (kAnd) {
-          ph_lo[r] = ph_lo[r - 1];
+#pragma unroll
+          for (int q = 0; q < NPH; ++q) ph[r][q] = ph[r - 1][q];
         } else {
 #pragma unroll
           for (int j = 0; j < kW; ++j) win[r][j] = win[r - 1][j];

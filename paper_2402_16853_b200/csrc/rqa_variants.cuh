@@ -27,7 +27,7 @@ constexpr int min_blocks() {
 
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
-  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8);
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>);
   auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(), PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
@@ -38,7 +38,7 @@ cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8);
+  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>);
   return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total,
                  &launch_unit<METRIC, M, TAU, NW, R, PREC>,
                  (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(),

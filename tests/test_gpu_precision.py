@@ -159,7 +159,8 @@ rng = np.random.default_rng(23)
 for kind, m, tau, metric, r, w in (("uniform", 3, 1, "l2", 0.1, 0), ("uniform", 2, 3, "l2", 0.05, 1),
                                    ("sine", 2, 1, "l2", 0.5, 0), ("uniform", 5, 1, "l2", 0.3, 2),
                                    ("uniform", 3, 1, "l1", 0.2, 0), ("sine", 2, 2, "l1", 1.0, 0),
-                                   ("uniform", 4, 2, "l2", 0.25, 0)):
+                                   ("uniform", 4, 2, "l2", 0.25, 0), ("sine", 10, 5, "l1", 3.0, 10),
+                                   ("sine", 5, 5, "l2", 0.8, 1)):
     n = 3100
     s = rng.uniform(0, 1, n) if kind == "uniform" else np.sin(np.linspace(0, 60, n)) + 0.1 * rng.normal(size=n)
     s[100] = np.nan
