@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 300 python scripts/time_configs.py C4 C3 > gpurun_out/q_time.log 2>&1; cat gpurun_out/q_time.log
-RQA_PREFILTER=0 timeout 300 python scripts/time_configs.py C4 > gpurun_out/q_time0.log 2>&1; cat gpurun_out/q_time0.log
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/q_all.log 2>&1; tail -2 gpurun_out/q_all.log
+timeout 1200 python scripts/stripe_projection.py C5 > gpurun_out/proj_C5.log 2>&1; tail -3 gpurun_out/proj_C5.log | cut -c1-250
+cp gpurun_out/stripe_projection.json gpurun_out/stripe_projection_C5.json
