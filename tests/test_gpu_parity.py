@@ -238,3 +238,33 @@ def test_largest_embedding_window(oracle_lib):
         st = AnalysisSettings(m, tau, "l1", r)
         want = oracle_lib.oracle_histograms(s, m, tau, "l1", r, 0, tile_size=128)
         assert_same(gpu_hist(s, st), want, f"m{m} t{tau}")
+
+
+def test_c_abi_dense_and_sparse_outputs_agree(oracle_lib):
+    """rqa_run (dense copy-back, the reference binding of INTEGRATION.md) and
+    rqa_run_prec with RQA_FLAG_OUT_ZEROED (device-compacted bins) agree with
+    the oracle; garbage in the output arrays is overwritten by rqa_run."""
+    import ctypes
+
+    from paper_2402_16853_b200 import _native
+
+    rng = np.random.default_rng(12)
+    s = rng.uniform(0, 1, 3000)
+    n = 3000 - 2
+    want = oracle_lib.oracle_histograms(s, 3, 1, "l2", 0.15, 1, tile_size=256)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    pd = ctypes.POINTER(ctypes.c_double)
+    d, v, w = (np.full(n + 1, 77, np.int64) for _ in range(3))
+    pts = np.zeros(1, np.int64)
+    tim = np.zeros(_native.TIMING_SLOTS)
+    _native.call("rqa_run", s.ctypes.data_as(pd), s.shape[0], 3, 1, 1, 0.15, 1, 0,
+                 d.ctypes.data_as(p64), v.ctypes.data_as(p64), w.ctypes.data_as(p64),
+                 pts.ctypes.data_as(p64), tim.ctypes.data_as(pd))
+    assert_same((d, v, w, int(pts[0])), want, "rqa_run dense")
+    d2, v2, w2 = (np.zeros(n + 1, np.int64) for _ in range(3))
+    pts2 = np.zeros(1, np.int64)
+    mism = np.zeros(1, np.int64)
+    _native.call("rqa_run_prec", s.ctypes.data_as(pd), s.shape[0], 3, 1, 1, 0.15, 1, 64, 0, 1,
+                 d2.ctypes.data_as(p64), v2.ctypes.data_as(p64), w2.ctypes.data_as(p64),
+                 pts2.ctypes.data_as(p64), mism.ctypes.data_as(p64), tim.ctypes.data_as(pd))
+    assert_same((d2, v2, w2, int(pts2[0])), want, "rqa_run_prec sparse")
