@@ -196,3 +196,39 @@ def test_prefilter_chosen_for_sparse_c3_like(oracle_lib):
         assert timing["evaluation"] == "fp64-prefilter"
     want = oracle_lib.oracle_histograms(s, 3, 1, "l2", 0.1, 0, tile_size=512)
     assert_same((h.diagonal, h.vertical, h.white_vertical, h.recurrence_points), want, "C3-like")
+
+
+def test_fp32_stripes_then_stitch_equal_single_run():
+    """fp32 mode through the device-resident stripe path (multi-GPU building
+    blocks): histograms and the summed mismatch counts equal the single run."""
+    import torch
+
+    from paper_2402_16853_b200.device import (MODE_FINAL, MODE_STRIPE, StripeOutputs,
+                                              band_rows, run_rows_device, stitch_device)
+    from paper_2402_16853_b200.distributed import stripe_bounds
+
+    rng = np.random.default_rng(31)
+    s = 100.0 + rng.uniform(0, 1e-3, 7000)
+    st = AnalysisSettings(2, 1, "l2", 2e-4)
+    n = 7000 - 1
+    dev = torch.device("cuda", 0)
+    sd = torch.from_numpy(s).to(dev)
+    ref_h = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
+    ref_p = torch.zeros(1, dtype=torch.int64, device=dev)
+    ref_m = torch.zeros(1, dtype=torch.int64, device=dev)
+    run_rows_device(sd, st, 0, n, MODE_FINAL, ref_h, ref_p, precision="fp32", mismatches=ref_m)
+    for g in (2, 3):
+        bounds = stripe_bounds(n, g, band_rows(st, n))
+        h = torch.zeros_like(ref_h)
+        p = torch.zeros_like(ref_p)
+        mm = torch.zeros_like(ref_m)
+        gathered = StripeOutputs.empty(n, dev, rows=g)
+        for q in range(g):
+            so = StripeOutputs(gathered.prefix[q], gathered.suffix[q], gathered.col[q],
+                               gathered.rowlead)
+            run_rows_device(sd, st, bounds[q], bounds[q + 1], MODE_STRIPE, h, p, so,
+                            precision="fp32", mismatches=mm)
+        stitch_device(gathered, bounds, n, h)
+        torch.cuda.synchronize()
+        assert torch.equal(h, ref_h) and torch.equal(p, ref_p) and torch.equal(mm, ref_m), g
+    assert int(ref_m.item()) > 0
