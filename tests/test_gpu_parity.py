@@ -268,3 +268,49 @@ def test_c_abi_dense_and_sparse_outputs_agree(oracle_lib):
                  d2.ctypes.data_as(p64), v2.ctypes.data_as(p64), w2.ctypes.data_as(p64),
                  pts2.ctypes.data_as(p64), mism.ctypes.data_as(p64), tim.ctypes.data_as(pd))
     assert_same((d2, v2, w2, int(pts2[0])), want, "rqa_run_prec sparse")
+
+
+ADVERSARIAL = [
+    # (name, series builder, m, tau, metric, radius)
+    ("grid-ties-l2", lambda r: np.round(r.uniform(0, 8, 1500)) * 0.25, 2, 1, "l2", 0.25 * 2 ** 0.5),
+    ("grid-ties-l1", lambda r: np.round(r.uniform(0, 8, 1500)) * 0.5, 3, 1, "l1", 1.0),
+    ("grid-ties-linf", lambda r: np.round(r.uniform(0, 8, 1500)) * 0.5, 3, 2, "linf", 0.5),
+    ("radius-zero", lambda r: np.round(r.uniform(0, 3, 1200)), 2, 1, "l2", 0.0),
+    ("denormals", lambda r: r.uniform(0, 1, 1300) * 5e-324 * 1000, 3, 1, "l2", 5e-322),
+    ("tiny-radius-l2", lambda r: r.uniform(0, 1, 1300) * 1e-160, 3, 1, "l2", 1e-161),
+    ("huge-overflow", lambda r: r.uniform(-1, 1, 1300) * 1e300, 3, 1, "l2", 1e300),
+    ("huge-radius", lambda r: r.uniform(-1, 1, 1300) * 1e300, 2, 1, "l2", 1.7e308),
+    ("inf-radius", lambda r: r.uniform(-1, 1, 900), 3, 1, "l1", float("inf")),
+    ("signed-zeros", lambda r: np.where(r.random(1000) < 0.5, -0.0, 0.0), 3, 1, "linf", 0.0),
+    ("constant", lambda r: np.full(1100, 3.25), 4, 2, "l2", 0.0),
+    ("nan-and-inf", lambda r: np.where(r.random(1200) < 0.02, np.inf,
+                                       np.where(r.random(1200) < 0.02, np.nan,
+                                                r.uniform(0, 1, 1200))), 3, 1, "l2", 0.3),
+]
+
+
+@pytest.mark.parametrize("case", ADVERSARIAL, ids=[c[0] for c in ADVERSARIAL])
+def test_adversarial_inputs_vs_oracle(case, oracle_lib):
+    """Ties exactly at the radius, denormals, overflowing squares, radius 0 /
+    huge / inf, signed zeros, non-finite samples: bit-exact on every path."""
+    name, build, m, tau, metric, radius = case
+    s = build(np.random.default_rng(len(name)))
+    for w in (0, 1):
+        st = AnalysisSettings(m, tau, metric, radius, theiler_corrector=w)
+        want = oracle_lib.oracle_histograms(s, m, tau, metric, radius, w, tile_size=128)
+        assert_same(gpu_hist(s, st), want, f"{name} w{w}")
+
+
+@pytest.mark.parametrize("case", ADVERSARIAL, ids=[c[0] for c in ADVERSARIAL])
+def test_adversarial_inputs_fp32_mode(case, oracle_lib):
+    """The same inputs in fp32 mode: float32 histograms and the exact
+    fp32/fp64 mismatch count (band certification off for most of them)."""
+    name, build, m, tau, metric, radius = case
+    s = build(np.random.default_rng(len(name)))
+    st = AnalysisSettings(m, tau, metric, radius)
+    h, t = run_analysis(embed(s, m, tau), st, precision="fp32")
+    d, v, w, p, mism = oracle_lib.oracle_histograms_prec(s, m, tau, metric, radius, 0,
+                                                         precision=32, tile_size=128)
+    assert_same((h.diagonal, h.vertical, h.white_vertical, h.recurrence_points), (d, v, w, p),
+                f"fp32 {name}")
+    assert t["mismatched_cells"] == mism, (name, t["mismatched_cells"], mism)
