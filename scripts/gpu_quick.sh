@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python scripts/fuzz_parity.py 4000 7 > gpurun_out/fuzz.log 2>&1; tail -1 gpurun_out/fuzz.log | cut -c1-400; cp gpurun_out/fuzz_parity.json gpurun_out/fuzz_parity_default.json
-RQA_PREFILTER=1 timeout 1500 python scripts/fuzz_parity.py 2000 8 > gpurun_out/fuzz1.log 2>&1; tail -1 gpurun_out/fuzz1.log | cut -c1-400; cp gpurun_out/fuzz_parity.json gpurun_out/fuzz_parity_prefilter.json
-RQA_FILTER=2 timeout 1500 python scripts/fuzz_parity.py 2000 9 > gpurun_out/fuzz2.log 2>&1; tail -1 gpurun_out/fuzz2.log | cut -c1-400; cp gpurun_out/fuzz_parity.json gpurun_out/fuzz_parity_f32filter.json
+for wl in P C4 C2; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:unit_kernel -s 1 -c 1 -o gpurun_out/prof_${wl} python scripts/profile_once.py $wl 2 > gpurun_out/prof_${wl}.log 2>&1; tail -1 gpurun_out/prof_${wl}.log
+done
