@@ -388,6 +388,8 @@ int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
   if (want == 0) return RQA_OK;
   Variant pv;
   if (!find_variant_pre(p->metric, p->m, p->tau, &pv)) return RQA_OK;
+  // small matrices: the sampling round trip would cost more than it can save
+  if (want != 1 && p->n < ((int64_t)1 << 15)) return RQA_OK;
   const double dstar = prefilter_bound(p->metric, p->thr);
   if (!(dstar >= 0) || std::isinf(dstar)) return RQA_OK;
   if (want != 1) {
@@ -435,7 +437,13 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   // iteration per unit boundary
   static const char* wenv = getenv("RQA_WAVES");
   const int64_t waves = wenv ? std::max(1, atoi(wenv)) : 16;
-  int64_t len = std::max<int64_t>(8, total / std::max<int64_t>(1, waves * slots));
+  // units of >= 16 iterations keep the recomputed iteration <= 1/16 of the
+  // work, unless the whole triangle is too small to fill the GPU once (C1):
+  // then parallelism wins over the recomputation
+  static const char* menv = getenv("RQA_MIN_UNIT");
+  const int64_t min_len = menv ? std::max(1, atoi(menv))
+                               : std::min<int64_t>(16, std::max<int64_t>(1, total / slots));
+  int64_t len = std::max<int64_t>(min_len, total / std::max<int64_t>(1, waves * slots));
   UnitPlan pl;
   pl.band_start.assign(nb + 1, 0);
   for (int64_t b = 0; b < nb; ++b) {
