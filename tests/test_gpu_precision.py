@@ -189,7 +189,7 @@ def test_prefilter_modes_in_subprocess(mode, expect):
 
 def test_prefilter_chosen_for_sparse_c3_like(oracle_lib):
     rng = np.random.default_rng(8)
-    s = rng.uniform(0, 1, 6000)
+    s = rng.uniform(0, 1, 40000)   # >= 2^15 vectors: the prefilter is sampled
     st = AnalysisSettings(3, 1, "l2", 0.1)
     h, timing = run_analysis(embed(s, 3, 1), st)
     if "RQA_PREFILTER" not in os.environ:
