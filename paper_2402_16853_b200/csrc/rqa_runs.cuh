@@ -116,7 +116,10 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 // histogram updates run at full SIMD width even when only a few lanes of a
 // pass see a boundary.
 // ---------------------------------------------------------------------------
-constexpr int kQueueCap = 128;  // events per warp (uint4 each); drained at >= 32
+constexpr int kQueueCap = 128;  // events per warp (uint4 each)
+// Drain when this many events are queued: every check follows at most 64
+// pushes (two words per lane), so the ring never holds more than 127.
+constexpr uint32_t kDrainAt = 64u;
 
 // Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
 // bit 0 skip the carried run (it is the sequence's first run, kept in the
@@ -219,7 +222,7 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
 __device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
                                           EventQueue& q, const Hist& h, int lane) {
   runs_push(x, nb, st, diag_weight, q);
-  if (q.tail - q.head >= 32u) queue_drain(q, h, lane, false);
+  if (q.tail - q.head >= kDrainAt) queue_drain(q, h, lane, false);
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {

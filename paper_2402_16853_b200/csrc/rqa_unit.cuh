@@ -592,7 +592,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               pts += __popc(w);
               runs_push(w, 32, rs[p], 0u, evq);
             }
-            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
           }
         } else {
 #pragma unroll 1
@@ -604,7 +604,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               pts += __popc(w);
               runs_push(w, nb, rs[p], 0u, evq);
             }
-            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
           }
         }
 #pragma unroll
@@ -663,7 +663,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
                 runs_push(bits, nb, cur[p], 0u, evq);
               }
             }
-            if (evq.tail - evq.head >= 32u) queue_drain(evq, hist, lane, false);
+            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
           };
           using kFull = std::integral_constant<bool, true>;
           using kPart = std::integral_constant<bool, false>;
