@@ -457,7 +457,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
           for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
           ph[r][NPH - 1] = 0u;
-          dw[r] = w;
+          dw[r] = kdr[r] < theiler ? 0u : w;  // Theiler-excluded cells need no sum
         }
         constexpr int RB = (R >= 2) ? 2 : 1;  // slots per cooperative batch
         uint16_t* cl = reinterpret_cast<uint16_t*>(smem + L.off_cand) + wv * kCandCap;
@@ -528,7 +528,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           ph[r][NPH - 1] = 0u;
           if constexpr (kPre && !kCoopResolve<PREC, M>) {
             // exact sums (reference order) for the candidate cells only
-            uint32_t cand = word, res = 0u;
+            uint32_t cand = kdr[r] < theiler ? 0u : word, res = 0u;
             while (cand) {
               const int t = __ffs(cand) - 1;
               cand &= cand - 1u;
