@@ -308,6 +308,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       lastc[r] = crows;
       openb[r] = (crows == vrows) ? 1 : 0;
     }
+    // slots whose 32 diagonals all run through all HS rows: every word of the
+    // iteration is a full 32-bit pass (warp-uniform fast path of the diagonal runs)
+    uint32_t fullmask = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (__all_sync(0xffffffffu, kdr[r] >= 0 && kdr[r] < nrem && lastc[r] == HS))
+        fullmask |= 1u << r;
 
     for (int c = 0; c < NCH; ++c) {
       uint32_t dw[R];
@@ -541,7 +548,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
         const int kd = kdr[r];
         if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-        if (!warm && !(a.skip & 1)) {
+        if (!warm && !(a.skip & 1) && ((fullmask >> r) & 1u)) {
+          runs_pass(word, 32, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
+        } else if (!warm && !(a.skip & 1)) {
           const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
           runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
