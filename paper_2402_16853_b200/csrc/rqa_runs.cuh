@@ -210,12 +210,15 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
   st.first = mkfirst ? cur + (p1 << 1) : st.first;
   st.cur = ev ? cur_ev : cur + ((uint32_t)nb << 1);
   const uint32_t m = __ballot_sync(0xffffffffu, ev);
-  if (ev) {  // 32-bit shared address: no generic-address rematerialisation per push
-    const uint32_t slot = (q.tail + __popc(m & q.lt_mask)) & (uint32_t)(kQueueCap - 1);
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(q.ring_sa + 16u * slot),
-                 "r"(bnd), "r"(cur), "r"((diag_weight << 1) | (mkfirst ? 1u : 0u)), "r"(0u)
-                 : "memory");
-  }
+  // predicated store through a 32-bit shared address: no divergent branch and
+  // no generic-address rematerialisation per push
+  const uint32_t slot = (q.tail + __popc(m & q.lt_mask)) & (uint32_t)(kQueueCap - 1);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+      "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(q.ring_sa + 16u * slot),
+      "r"(bnd), "r"(cur), "r"((diag_weight << 1) | (mkfirst ? 1u : 0u)), "r"(0u),
+      "r"(ev ? 1u : 0u)
+      : "memory");
   q.tail += __popc(m);
 }
 
