@@ -126,14 +126,19 @@ constexpr uint32_t kDrainAt = 64u;
 // state), bits 1..2 diagonal weight (0: vertical/white sink).
 __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint32_t len,
                                          uint32_t w) {
-  // len < kSmemBins: 32-bit shared bin; else 64-bit global counter
+  // len < kSmemBins: 32-bit shared bin; else 64-bit global counter; w == 0:
+  // nothing (predicated, so callers need no branch)
   const uint32_t sa = h.sh + 4u * (kind_row * (uint32_t)kSmemBins + len);
   unsigned long long* ga = h.g + (int64_t)kind_row * h.stride + len;
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, q, s, g;\n\t"
       "setp.lt.u32 p, %0, %4;\n\t"
-      "@p red.shared.add.u32 [%1], %3;\n\t"
-      "@!p red.global.add.u64 [%2], %5;\n\t}" ::"r"(len),
+      "setp.ne.u32 q, %3, 0;\n\t"
+      "and.pred s, p, q;\n\t"
+      "not.pred p, p;\n\t"
+      "and.pred g, p, q;\n\t"
+      "@s red.shared.add.u32 [%1], %3;\n\t"
+      "@g red.global.add.u64 [%2], %5;\n\t}" ::"r"(len),
       "r"(sa), "l"(ga), "r"(w), "n"(kSmemBins), "l"((unsigned long long)w)
       : "memory");
 }
@@ -150,7 +155,7 @@ __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
   uint32_t len = (e.y >> 1) + p;
   uint32_t wt = (e.z & 1u) ? 0u : (bit ? w1 : w0);
   for (;;) {
-    if (wt) hist_red(h, bit ? k1 : k0, len, wt);
+    hist_red(h, bit ? k1 : k0, len, wt);  // wt == 0: predicated off
     bnd &= bnd - 1u;
     if (bnd == 0u) break;
     const uint32_t q = (uint32_t)__ffs(bnd) - 1u;
@@ -172,13 +177,20 @@ struct EventQueue {
 // Expand whole groups of 32 events (all = true: everything left).  Kept out
 // of line: it runs once per ~10 passes and would otherwise be inlined at
 // every pass site.
-static __device__ __noinline__ uint32_t queue_drain_impl(const uint4* ring, uint32_t head, uint32_t tail,
-                                                  uint32_t sh, unsigned long long* g,
-                                                  int64_t stride, int lane, bool all) {
+static __device__ __noinline__ uint32_t queue_drain_impl(uint32_t ring_sa, uint32_t head,
+                                                         uint32_t tail, uint32_t sh,
+                                                         unsigned long long* g, int64_t stride,
+                                                         int lane, bool all) {
   const Hist h{sh, g, stride};
   while (tail - head >= 32u || (all && tail != head)) {
     const uint32_t avail = tail - head;
-    if ((uint32_t)lane < avail) expand_event(ring[(head + lane) % kQueueCap], h);
+    if ((uint32_t)lane < avail) {
+      uint4 e;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                   : "r"(ring_sa + 16u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
+      expand_event(e, h);
+    }
     head += avail < 32u ? avail : 32u;
   }
   __syncwarp();
@@ -187,7 +199,7 @@ static __device__ __noinline__ uint32_t queue_drain_impl(const uint4* ring, uint
 
 __device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int lane, bool all) {
   __syncwarp();
-  q.head = queue_drain_impl(q.ring, q.head, q.tail, h.sh, h.g, h.stride, lane, all);
+  q.head = queue_drain_impl(q.ring_sa, q.head, q.tail, h.sh, h.g, h.stride, lane, all);
 }
 
 // One pass: consume nb (0..32) bits of x, bit 0 first, into the lane's run
