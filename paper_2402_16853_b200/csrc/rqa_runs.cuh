@@ -124,23 +124,19 @@ constexpr uint32_t kDrainAt = 64u;
 // Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
 // bit 0 skip the carried run (it is the sequence's first run, kept in the
 // state), bits 1..2 diagonal weight (0: vertical/white sink).
+// Shared word just past the histogram bins and the kernel's two mbarriers
+// (SymSmem reserves it): the target of the zero-weight / out-of-range adds.
+constexpr uint32_t kDummyBin = 3u * kSmemBins + 4u;
+
 __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint32_t len,
                                          uint32_t w) {
-  // len < kSmemBins: 32-bit shared bin; else 64-bit global counter; w == 0:
-  // nothing (predicated, so callers need no branch)
-  const uint32_t sa = h.sh + 4u * (kind_row * (uint32_t)kSmemBins + len);
-  unsigned long long* ga = h.g + (int64_t)kind_row * h.stride + len;
-  asm volatile(
-      "{\n\t.reg .pred p, q, s, g;\n\t"
-      "setp.lt.u32 p, %0, %4;\n\t"
-      "setp.ne.u32 q, %3, 0;\n\t"
-      "and.pred s, p, q;\n\t"
-      "not.pred p, p;\n\t"
-      "and.pred g, p, q;\n\t"
-      "@s red.shared.add.u32 [%1], %3;\n\t"
-      "@g red.global.add.u64 [%2], %5;\n\t}" ::"r"(len),
-      "r"(sa), "l"(ga), "r"(w), "n"(kSmemBins), "l"((unsigned long long)w)
-      : "memory");
+  // len < kSmemBins: 32-bit shared bin, unconditionally (a zero weight adds 0),
+  // so ptxas emits no branch around it; longer lines go to the 64-bit global
+  // counter in a rarely taken branch (the shared add then hits a dummy word)
+  const bool small = len < (uint32_t)kSmemBins;
+  const uint32_t sa = h.sh + 4u * (small ? kind_row * (uint32_t)kSmemBins + len : kDummyBin);
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa), "r"(small ? w : 0u) : "memory");
+  if (!small && w) atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
 }
 
 __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {

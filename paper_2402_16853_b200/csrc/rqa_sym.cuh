@@ -95,7 +95,8 @@ struct SymSmem {
     off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
     off_queue = off_rowst + (size_t)R * D * sizeof(uint2);
     off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
-    off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 16;  // after the mbarriers
+    // bins, two mbarriers (16 B), the dummy bin of hist_red (16 B reserved)
+    off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
     off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
     total = off_cres + (coop ? (size_t)NW * R * 32 * sizeof(uint32_t) : 0);
   }
