@@ -654,7 +654,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
           // shifted into aligned columns, transposed, met bottom-up
           // 32-bit shared addresses of the row words (rowbuf / previous iteration)
-          const uint32_t rb_sa = smem_u32(rowbuf), pv_sa = smem_u32(prev_cur);
+          uint32_t rb_sa = smem_u32(rowbuf), pv_sa = smem_u32(prev_cur);
+          asm volatile("" : "+r"(rb_sa), "+r"(pv_sa));  // keep in registers (no re-derivation)
           auto col_step = [&](int c, const int* lim, auto full) {
             const int wp = (wv - c) & (NW - 1);
 #pragma unroll
