@@ -3,7 +3,7 @@
 Draws random (family, n, m, tau, metric, radius quantile, Theiler window,
 precision, device list) cases, runs run_analysis and the oracle on the same
 series, and requires bit-identical histograms and point counts (and, for
-fp32 mode, the same mismatch count).  Usage: python scripts/fuzz_parity.py [CASES] [SEED]
+fp32 mode, the same mismatch count).  Usage: python scripts/fuzz_parity.py [CASES] [SEED] [MAX_LEN]
 """
 import json
 import os
@@ -18,10 +18,11 @@ from paper_2402_16853_b200 import AnalysisSettings, distance, embed, run_analysi
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2026)
+max_len = int(sys.argv[3]) if len(sys.argv) > 3 else 6000  # series length bound
 fails, t0, stats = [], time.time(), {}
 for i in range(cases):
     fam = rng.choice(["uniform", "sine", "ar1", "offset", "grid"])
-    n_len = int(rng.integers(20, 6000))
+    n_len = int(rng.integers(20, max_len))
     m = int(rng.choice([1, 2, 3, 4, 5, 6, 10]))
     tau = int(rng.choice([1, 2, 3, 5]))
     if n_len <= (m - 1) * tau + 1:
