@@ -186,6 +186,11 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   uint2* piece = ua.rowpiece + (int64_t)unit.idx * H;
   const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
   const Transposer tr(lane);
+  // this lane's row-word slot (warp wv, row lane of chunk 0, slot 0) as a
+  // 32-bit shared address kept in a register; profiling mask likewise
+  uint32_t rowbuf_sa = smem_u32(rowbuf + wv * H + lane);
+  int skip = a.skip;
+  asm volatile("" : "+r"(rowbuf_sa), "+r"(skip));
   EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
   evq.ring_sa = smem_u32(evq.ring);
@@ -548,9 +553,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
         const int kd = kdr[r];
         if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-        if (!warm && !(a.skip & 1) && ((fullmask >> r) & 1u)) {
+        if (!warm && !(skip & 1) && ((fullmask >> r) & 1u)) {
           runs_pass(word, 32, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
-        } else if (!warm && !(a.skip & 1)) {
+        } else if (!warm && !(skip & 1)) {
           const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
           runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
@@ -562,7 +567,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
             st[r] = RunState{1u, 0u};
           }
         }
-        rowbuf[wv * H + r * HS + 32 * c + lane] = tr(word);
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
+                     "r"(tr(word))
+                     : "memory");
       }
     }
     __syncthreads();
@@ -586,7 +593,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         any_rem |= rem[p] > 0;
         all_full &= rem[p] >= D;
       }
-      if (!(a.skip & 2) && __any_sync(0xffffffffu, any_rem)) {
+      if (!(skip & 2) && __any_sync(0xffffffffu, any_rem)) {
 #pragma unroll
         for (int p = 0; p < PR; ++p) {
           const uint2 rsv = rowst[lr[p]];
@@ -650,7 +657,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           lim_fin[p] = (do_fin && x >= r && cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
           lim_new[p] = (do_new && x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
         }
-        if (!(a.skip & 4) && x >= rs_[PR - 1]) {
+        if (!(skip & 4) && x >= rs_[PR - 1]) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
           // shifted into aligned columns, transposed, met bottom-up
           // 32-bit shared addresses of the row words (rowbuf / previous iteration)
