@@ -102,36 +102,74 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference(settings, series_full, n_full, budget_s=20.0, threads=None):
-    """Time the oracle port (CPU restatement of tiledrqa) on a prefix sample.
+def cpu_model() -> str:
+    """`lscpu` model name of the host (BASELINE.md's CPU-baseline record)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    Grows the prefix until one run takes >= budget_s/4, then reports the
-    cells/s of the largest run (bounded to ~budget_s of CPU work overall).
+
+CPU_PREFIX = 131_072  # vectors of the CPU sample, the same in both arms
+
+
+def cpu_reference(settings, series_full, n_full, prefix=CPU_PREFIX, threads=None):
+    """Time the oracle port (C restatement of tiledrqa's run_analysis, all
+    host threads) on the first ``prefix`` vectors of the same series.
+
+    Both bench arms (this line's cpu_baseline and ``--impl reference``) use
+    this function with the same prefix, so their CPU numbers are comparable.
     """
     from oracle.oracle import oracle_histograms
 
     threads = threads or len(os.sched_getaffinity(0))
     m, tau = settings.embedding_dimension, settings.time_delay
     span = (m - 1) * tau
-    n = 4096
-    best = None
-    spent = 0.0
-    while True:
-        n = min(n, n_full)
-        s = series_full[: n + span]
-        t0 = time.perf_counter()
-        oracle_histograms(s, m, tau, settings.metric, settings.radius, settings.theiler_window,
-                          tile_size=1024, workers=threads)
-        dt = time.perf_counter() - t0
-        spent += dt
-        best = (n, dt)
-        if dt >= budget_s / 4 or n >= n_full or spent + 4.5 * dt > budget_s:
-            break
-        n *= 2
-    n, dt = best
+    n = min(prefix, n_full)
+    s = series_full[: n + span]
+    t0 = time.perf_counter()
+    oracle_histograms(s, m, tau, settings.metric, settings.radius, settings.theiler_window,
+                      tile_size=1024, workers=threads)
+    dt = time.perf_counter() - t0
     return {"value": n * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(), "threads": threads,
             "sample": f"prefix of {n} vectors ({n * n:.3e} cells) of the same series, "
-                      f"{dt:.2f} s, oracle/rqa_oracle.c tiled port, tile 1024"}
+                      f"{dt:.2f} s, oracle/rqa_oracle.c tiled port (tile 1024, "
+                      f"{threads} threads)"}
+
+
+def golden_parity(workload, hist_np, points):
+    """Compare the final histograms with tests/golden/full_<workload>.json
+    (made by tests/golden/make_full_golden.py from the pinned oracle)."""
+    path = os.path.join(REPO, "tests", "golden", f"full_{workload}.json")
+    if not os.path.exists(path):
+        return "no golden"
+    with open(path) as fh:
+        fx = json.load(fh)
+    res = fx["result"]
+    n = res["n_vectors"]
+    if hist_np.shape[1] != n + 1:
+        return "mismatch (size)"
+    if int(points) != int(res["recurrence_points"]):
+        return "mismatch (points)"
+    for row, key in enumerate(("diagonal", "vertical", "white_vertical")):
+        want = np.zeros(n + 1, np.int64)
+        for k, v in res[key].items():
+            want[int(k)] = v
+        if not np.array_equal(hist_np[row], want):
+            return f"mismatch ({key})"
+    return "exact"
 
 
 def flush_l2(buf):
@@ -146,7 +184,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-prefix", type=int, default=CPU_PREFIX)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     args = ap.parse_args()
 
     from paper_2402_16853_b200.workloads import WORKLOADS, series_sha256
@@ -170,8 +209,7 @@ def main():
         per_step = []
         info = None
         for i in range(args.warmup + args.steps):
-            info = cpu_reference(settings, series, n_full,
-                                 budget_s=max(4.0, 60.0 / (args.warmup + args.steps)))
+            info = cpu_reference(settings, series, n_full, prefix=args.cpu_prefix)
             if i >= args.warmup:
                 per_step.append(info["value"])
         val = float(np.median(per_step))
@@ -182,7 +220,8 @@ def main():
                "data": "synthetic (seeded, sha256 " + series_sha256(series)[:16] + ")",
                "config": config,
                "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"],
-                                "kind": "port", "sample": info["sample"]},
+                                "kind": "port", "sample": info["sample"],
+                                "cpu_model": info["cpu_model"], "threads": info["threads"]},
                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0},
                "note": "ms_per_step is the N^2-extrapolated wall of the full workload"}
@@ -221,6 +260,8 @@ def main():
     series = torch.from_numpy(series_np).to(dev)
     hist = torch.zeros(3, n + 1, dtype=torch.int64, device=dev)
     points = torch.zeros(1, dtype=torch.int64, device=dev)
+    prec = args.precision
+    mism = torch.zeros(1, dtype=torch.int64, device=dev) if prec == "fp32" else None
     so = StripeOutputs.empty(n, dev) if world > 1 else None
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -230,12 +271,15 @@ def main():
     def step():
         hist.zero_()
         points.zero_()
+        if mism is not None:
+            mism.zero_()
         if world == 1:
-            run_rows_device(series, settings, 0, n, MODE_FINAL, hist, points, stream=stream)
+            run_rows_device(series, settings, 0, n, MODE_FINAL, hist, points, stream=stream,
+                            precision=prec, mismatches=mism)
         else:
             so.rowlead.zero_()
             run_rows_device(series, settings, lo, hi, MODE_STRIPE, hist, points, so,
-                            stream=stream)
+                            stream=stream, precision=prec, mismatches=mism)
             gathered = exchange(so, world)
             reduce_sum(hist, 0)
             reduce_sum(points, 0)
@@ -264,6 +308,11 @@ def main():
             barrier()
             times.append(ev[0].elapsed_time(ev[1]) * 1e-3)
     launches = lib.rqa_launch_counter() - launches0
+    # parity self-check of the last timed step (untimed): bit-exact against
+    # the full-size golden of tests/golden (fp64) ...
+    parity = None
+    if rank == 0 and prec == "fp64":
+        parity = golden_parity(args.workload, hist.cpu().numpy(), int(points.item()))
     t_step = float(np.mean(times))
     if world > 1:
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
@@ -281,8 +330,10 @@ def main():
         flush_l2(flush)
         torch.cuda.synchronize()
         ev[0].record(stream)
+        if mism is not None:
+            mism.zero_()
         run_rows_device(series, settings, lo, hi, MODE_FINAL if world == 1 else MODE_STRIPE,
-                        hist, points, so, stream=stream)
+                        hist, points, so, stream=stream, precision=prec, mismatches=mism)
         ev[1].record(stream)
         torch.cuda.synchronize()
         kern_times.append(ev[0].elapsed_time(ev[1]) * 1e-3)
@@ -301,18 +352,18 @@ def main():
 
         emb = embed(series_np, settings.embedding_dimension, settings.time_delay)
         dev_index = torch.cuda.current_device()
-        _, e2e_timing = run_analysis(emb, settings, device=dev_index)
+        _, e2e_timing = run_analysis(emb, settings, device=dev_index, precision=prec)
         e2e_t = []
         for _ in range(max(1, args.steps)):
             flush_l2(flush)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            analyze(series_np, settings, device=dev_index)
+            analyze(series_np, settings, device=dev_index, precision=prec)
             e2e_t.append(time.perf_counter() - t0)
         e2e_val = cells / float(np.mean(e2e_t))
         # results come back as device-compacted nonzero bins (16 B each) plus
         # the counter and the point count (run_analysis, RQA_FLAG_OUT_ZEROED)
-        res_h = analyze(series_np, settings, device=dev_index).histograms
+        res_h = analyze(series_np, settings, device=dev_index, precision=prec).histograms
         nnz = sum(int(np.count_nonzero(a)) for a in (res_h.diagonal, res_h.vertical,
                                                      res_h.white_vertical))
         d2h = 16 * nnz + 8 + 8
@@ -342,8 +393,10 @@ def main():
     lib.rqa_fp64_peak(local, ctypes.byref(dadd), ctypes.byref(dmul), err, 256)
     peak = min(dadd.value, dmul.value)
     # cells of the full matrix that this rank's stripe accounts for (upper
-    # triangle rows [lo, hi) stand for their mirrored lower-triangle cells too)
+    # triangle rows [lo, hi) stand for their mirrored lower-triangle cells
+    # too) and the cells its kernel actually evaluates (the upper triangle)
     local_cells = float(n - lo + n - hi) * float(hi - lo)
+    evaluated_cells = float(n - lo + n - hi + 1) * float(hi - lo) / 2.0
     alg_ops = local_cells * ops_per_cell(settings)
     achieved = alg_ops / t_kern
     evaluation = e2e_timing.get("evaluation", "fp64") if world == 1 else "fp64"
@@ -382,9 +435,17 @@ def main():
         "kernel_s": t_kern,
         "algorithmic_ops_per_cell": ops_per_cell(settings),
         "evaluation": evaluation,
-        "executed_fp64_ops_per_cell": executed_ops_per_cell(settings, evaluation, cand),
-        "executed_frac": local_cells * executed_ops_per_cell(settings, evaluation, cand)
+        "frac_full_matrix": achieved / peak if peak else None,
+        "frac_per_evaluated_cell": evaluated_cells * ops_per_cell(settings) / t_kern / peak
+        if peak else None,
+        "evaluated_cells": evaluated_cells,
+        "executed_fp64_ops_per_evaluated_cell": executed_ops_per_cell(settings, evaluation, cand),
+        "executed_frac": evaluated_cells * executed_ops_per_cell(settings, evaluation, cand)
         / t_kern / peak if peak else None,
+        "note": "frac = frac_full_matrix: SURVEY 8d algorithmic ops over all N^2 cells; "
+                "the kernel evaluates only the upper triangle (R = R^T exactly), so "
+                "frac_per_evaluated_cell is the same ops over the cells evaluated; "
+                "executed_frac counts the FP64 ops the chosen kernel really issues",
     }
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
@@ -398,9 +459,21 @@ def main():
            "issue_roofline": issue,
            "clocks": clocks.summary(),
            "full_rqa_wall_s": cells / e2e_val if e2e_val else None,
-           "full_rqa": full_rqa}
+           "full_rqa": full_rqa,
+           "parity": parity,
+           "precision": prec}
+    if prec == "fp32" and world == 1:
+        from paper_2402_16853_b200 import compare_precision
+
+        rep = compare_precision(series_np, settings, device=dev_index)
+        out["fp32_mode"] = {"mismatched_cells": rep["mismatched_cells"],
+                            "mismatch_fraction": rep["mismatched_cells"] / rep["cells"],
+                            "max_rel_error": rep["max_rel_error"],
+                            "rel_error": rep["rel_error"],
+                            "evaluation": rep["fp32_evaluation"]}
+        out["dtype"] = "f32"
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_reference(settings, series_np, n, budget_s=args.cpu_budget)
+        out["cpu_baseline"] = cpu_reference(settings, series_np, n, prefix=args.cpu_prefix)
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

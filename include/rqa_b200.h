@@ -110,14 +110,18 @@ int rqa_run_prec(const double *series, int64_t len, int32_t m, int32_t tau, int3
  * are split into n_devices equal-area stripes of the upper triangle, one host
  * thread per stripe runs it on devices[g] (a device may appear more than
  * once), the stripe summaries are gathered on devices[0] by peer copies
- * (NVLink) and stitched there (rqa_stitch_device semantics); histograms and
- * counts are summed.  Results are identical to rqa_run_prec for every device
+ * (NVLink) and stitched there (rqa_stitch_device semantics); the stripes'
+ * histograms and counts are summed on devices[0] as well (peer copies plus a
+ * reduction kernel), so one (sparse, with RQA_FLAG_OUT_ZEROED) copy-back
+ * crosses PCIe.  Results are identical to rqa_run_prec for every device
  * list.  n_devices == 1 is rqa_run_prec.  Timing: [1] slowest stripe's
- * kernels, [2] stitch, [4] wall, [5] cells/s over the wall, [7] stripes.
+ * kernels, [2] gather + reduction + stitch, [4] wall, [5] cells/s over the
+ * wall, [6] band rows, [7] stripes, [8..10] as rqa_run_prec.
+ * Replaces the merge of per-worker partials, engine.py:271-276.
  */
 int rqa_run_multi(const double *series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                   double radius, int64_t theiler, int32_t precision, const int32_t *devices,
-                  int32_t n_devices, int64_t *diag, int64_t *vert, int64_t *white,
+                  int32_t n_devices, int32_t flags, int64_t *diag, int64_t *vert, int64_t *white,
                   int64_t *points, int64_t *mismatches, double *timing, char *err,
                   size_t errlen);
 

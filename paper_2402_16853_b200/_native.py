@@ -36,7 +36,7 @@ SYMBOLS = {
                                 _pi64, _pi64, _pi64, _pi64, _pi64, _pd, _c.c_char_p,
                                 _c.c_size_t]),
     "rqa_run_multi": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _pi32, _i32,
-                                 _pi64, _pi64, _pi64, _pi64, _pi64, _pd, _c.c_char_p,
+                                 _i32, _pi64, _pi64, _pi64, _pi64, _pi64, _pd, _c.c_char_p,
                                  _c.c_size_t]),
     "rqa_run_device_prec": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _i64,
                                        _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -277,6 +277,17 @@ __global__ void compact_bins_kernel(const unsigned long long* __restrict__ h, in
   }
 }
 
+// dst += src over count counters (multi-device histogram reduction on the
+// first device; src is a peer copy or another stripe's workspace there).
+__global__ void hist_accumulate_kernel(unsigned long long* __restrict__ dst,
+                                       const unsigned long long* __restrict__ src, int64_t count) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = src[q];
+    if (v) dst[q] += v;
+  }
+}
+
 __global__ void prep_f32_kernel(const double* __restrict__ s, float* __restrict__ sf, int64_t count,
                                 unsigned long long* maxbits) {
   unsigned long long mx = 0;
@@ -656,6 +667,59 @@ int run_full(Workspace* ws, const Problem& p, unsigned long long* hist, unsigned
   return stitch_stripes(ws, pre, suf, col, row, bounds.data(), g, p.n, hist, st, err, errlen);
 }
 
+// Results back to the caller: hist = [3][hn] histograms + points + mismatches
+// on the current device.  With RQA_FLAG_OUT_ZEROED (caller's arrays are
+// zero-filled) only the nonzero bins travel, compacted on the device; else
+// dense copies.  Synchronous on st.
+int copy_out(Workspace* ws, const unsigned long long* hist, size_t hn, int32_t flags, int64_t* diag,
+             int64_t* vert, int64_t* white, int64_t* points, int64_t* mismatches, cudaStream_t st,
+             char* err, size_t errlen) {
+  // outputs: the nonzero bins only when the caller's arrays are zero-filled
+  // (RQA_FLAG_OUT_ZEROED) and they fit the pair buffer, else dense copies
+  bool dense = true;
+  if (flags & RQA_FLAG_OUT_ZEROED) {
+    constexpr unsigned int kSparseCap = 1u << 20;
+    RQA_CUDA(grow(&ws->bins, &ws->bins_cap, 1 + 2 * (size_t)kSparseCap), "allocating bins");
+    unsigned int* counter = reinterpret_cast<unsigned int*>(ws->bins);
+    RQA_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st), "memset");
+    const int64_t nb3 = 3 * (int64_t)hn;
+    compact_bins_kernel<<<(int)std::min<int64_t>((nb3 + 255) / 256, 148 * 8), 256, 0, st>>>(
+        hist, nb3, ws->bins + 1, counter, kSparseCap);
+    RQA_CUDA(cudaGetLastError(), "launching bin compaction");
+    g_launches++;
+    unsigned long long cnt = 0;
+    RQA_CUDA(cudaMemcpyAsync(&cnt, ws->bins, sizeof cnt, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaStreamSynchronize(st), "bin compaction");
+    cnt &= 0xffffffffull;
+    if (cnt <= kSparseCap) {
+      std::vector<unsigned long long> pairs(2 * cnt + 2);
+      if (cnt)
+        RQA_CUDA(cudaMemcpyAsync(pairs.data(), ws->bins + 1, 2 * cnt * 8, cudaMemcpyDeviceToHost,
+                                 st),
+                 "d2h");
+      RQA_CUDA(cudaStreamSynchronize(st), "d2h");
+      int64_t* outs[3] = {diag, vert, white};
+      for (unsigned long long q = 0; q < cnt; ++q) {
+        const uint64_t idx = pairs[2 * q];
+        outs[idx / hn][idx % hn] = (int64_t)pairs[2 * q + 1];
+      }
+      dense = false;
+    }
+  }
+  if (dense) {
+    RQA_CUDA(cudaMemcpyAsync(diag, hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaMemcpyAsync(vert, hist + hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
+    RQA_CUDA(cudaMemcpyAsync(white, hist + 2 * hn, hn * 8, cudaMemcpyDeviceToHost, st),
+             "d2h");
+  }
+  RQA_CUDA(cudaMemcpyAsync(points, hist + 3 * hn, 8, cudaMemcpyDeviceToHost, st), "d2h");
+  if (mismatches)
+    RQA_CUDA(cudaMemcpyAsync(mismatches, hist + 3 * hn + 1, 8, cudaMemcpyDeviceToHost, st),
+             "d2h");
+  RQA_CUDA(cudaStreamSynchronize(st), "copying results");
+  return RQA_OK;
+}
+
 // FP64 pipe microbenchmark: 8 independent DADD (or DMUL) chains per thread.
 template <int OP>
 __global__ void fp64_peak_kernel(double* out, int iters, double a) {
@@ -685,6 +749,11 @@ struct StripeJob {
   float ms = 0.f;
   int rc = 0;
   char err[256] = {0};
+  // evaluation path the stripe's plan chose (timing[6], [8..10])
+  Variant var{};
+  int filt = -1;
+  float band32 = 0.f;
+  double cand = -1.0;
 };
 
 int run_stripe_job(StripeJob* j, const Problem& p0, const double* series) {
@@ -721,6 +790,10 @@ int run_stripe_job(StripeJob* j, const Problem& p0, const double* series) {
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[2], st), "event");
   RQA_CUDA(cudaStreamSynchronize(st), "stripe kernels");
+  j->var = p.var;
+  j->filt = p.filt;
+  j->band32 = p.band32;
+  j->cand = p.cand;
   cudaEventElapsedTime(&j->ms, ws->ev[1], ws->ev[2]);
   return RQA_OK;
 }
@@ -802,48 +875,8 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
   rc = run_full(ws, p, ws->hist, ws->hist + 3 * hn, st, ws->ev[2], err, errlen);
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[3], st), "event");
-  // outputs: the nonzero bins only when the caller's arrays are zero-filled
-  // (RQA_FLAG_OUT_ZEROED) and they fit the pair buffer, else dense copies
-  bool dense = true;
-  if (flags & RQA_FLAG_OUT_ZEROED) {
-    constexpr unsigned int kSparseCap = 1u << 20;
-    RQA_CUDA(grow(&ws->bins, &ws->bins_cap, 1 + 2 * (size_t)kSparseCap), "allocating bins");
-    unsigned int* counter = reinterpret_cast<unsigned int*>(ws->bins);
-    RQA_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st), "memset");
-    const int64_t nb3 = 3 * (int64_t)hn;
-    compact_bins_kernel<<<(int)std::min<int64_t>((nb3 + 255) / 256, 148 * 8), 256, 0, st>>>(
-        ws->hist, nb3, ws->bins + 1, counter, kSparseCap);
-    RQA_CUDA(cudaGetLastError(), "launching bin compaction");
-    g_launches++;
-    unsigned long long cnt = 0;
-    RQA_CUDA(cudaMemcpyAsync(&cnt, ws->bins, sizeof cnt, cudaMemcpyDeviceToHost, st), "d2h");
-    RQA_CUDA(cudaStreamSynchronize(st), "bin compaction");
-    cnt &= 0xffffffffull;
-    if (cnt <= kSparseCap) {
-      std::vector<unsigned long long> pairs(2 * cnt + 2);
-      if (cnt)
-        RQA_CUDA(cudaMemcpyAsync(pairs.data(), ws->bins + 1, 2 * cnt * 8, cudaMemcpyDeviceToHost,
-                                 st),
-                 "d2h");
-      RQA_CUDA(cudaStreamSynchronize(st), "d2h");
-      int64_t* outs[3] = {diag, vert, white};
-      for (unsigned long long q = 0; q < cnt; ++q) {
-        const uint64_t idx = pairs[2 * q];
-        outs[idx / hn][idx % hn] = (int64_t)pairs[2 * q + 1];
-      }
-      dense = false;
-    }
-  }
-  if (dense) {
-    RQA_CUDA(cudaMemcpyAsync(diag, ws->hist, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
-    RQA_CUDA(cudaMemcpyAsync(vert, ws->hist + hn, hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
-    RQA_CUDA(cudaMemcpyAsync(white, ws->hist + 2 * hn, hn * 8, cudaMemcpyDeviceToHost, st),
-             "d2h");
-  }
-  RQA_CUDA(cudaMemcpyAsync(points, ws->hist + 3 * hn, 8, cudaMemcpyDeviceToHost, st), "d2h");
-  if (mismatches)
-    RQA_CUDA(cudaMemcpyAsync(mismatches, ws->hist + 3 * hn + 1, 8, cudaMemcpyDeviceToHost, st),
-             "d2h");
+  rc = copy_out(ws, ws->hist, hn, flags, diag, vert, white, points, mismatches, st, err, errlen);
+  if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws->ev[4], st), "event");
   RQA_CUDA(cudaStreamSynchronize(st), "running kernels");
   if (timing) {
@@ -869,7 +902,7 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
 
 int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int32_t metric,
                   double radius, int64_t theiler, int32_t precision, const int32_t* devices,
-                  int32_t n_devices, int64_t* diag, int64_t* vert, int64_t* white,
+                  int32_t n_devices, int32_t flags, int64_t* diag, int64_t* vert, int64_t* white,
                   int64_t* points, int64_t* mismatches, double* timing, char* err,
                   size_t errlen) {
   if (!series || !diag || !vert || !white || !points || !devices)
@@ -889,12 +922,13 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
       return set_err(err, errlen, "device %d out of range (%d visible)", devices[g], ndev),
              RQA_EINVAL;
   if (n_devices == 1)
-    return rqa_run_prec(series, len, m, tau, metric, radius, theiler, precision, devices[0], 0,
-                        diag, vert, white, points, mismatches, timing, err, errlen);
+    return rqa_run_prec(series, len, m, tau, metric, radius, theiler, precision, devices[0],
+                        flags, diag, vert, white, points, mismatches, timing, err, errlen);
   const auto t0 = std::chrono::steady_clock::now();
   const int G = n_devices;
   const std::vector<int64_t> bounds = area_stripes(p.n, G, 1024);
   std::vector<StripeJob> jobs(G);
+  std::vector<std::unique_lock<std::mutex>> locks;
   for (int g = 0; g < G; ++g) {
     jobs[g].dev = devices[g];
     for (int q = 0; q < g; ++q) jobs[g].slot += devices[q] == devices[g];
@@ -902,9 +936,18 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
     jobs[g].hi = bounds[g + 1];
     jobs[g].ws = workspace(jobs[g].dev, jobs[g].slot);
   }
-  // every workspace is locked for the whole call (fixed order: no deadlock)
-  std::vector<std::unique_lock<std::mutex>> locks;
-  for (int g = 0; g < G; ++g) locks.emplace_back(jobs[g].ws->mu);
+  // every workspace is locked for the whole call, in one global order (the
+  // (slot, device) key): concurrent calls with permuted device lists cannot
+  // deadlock
+  {
+    std::vector<int> order(G);
+    for (int g = 0; g < G; ++g) order[g] = g;
+    std::sort(order.begin(), order.end(), [&](int x, int y) {
+      return jobs[x].slot * kMaxDevices + jobs[x].dev < jobs[y].slot * kMaxDevices + jobs[y].dev;
+    });
+    locks.reserve(G);
+    for (int g : order) locks.emplace_back(jobs[g].ws->mu);
+  }
   {
     std::vector<std::thread> th;
     for (int g = 0; g < G; ++g)
@@ -914,7 +957,9 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
   for (int g = 0; g < G; ++g)
     if (jobs[g].rc) return set_err(err, errlen, "device %d: %s", jobs[g].dev, jobs[g].err), jobs[g].rc;
 
-  // gather the stripe summaries on the first device and stitch there
+  // gather the stripe summaries and sum the histograms on the first device
+  // (peer copies over NVLink; stripes already on that device are added in
+  // place), stitch there, then one copy-back of the (sparse) result
   StripeJob& j0 = jobs[0];
   Workspace* ws0 = j0.ws;
   RQA_CUDA(cudaSetDevice(j0.dev), "cudaSetDevice");
@@ -925,13 +970,20 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
       if (can && cudaDeviceEnablePeerAccess(jobs[g].dev, 0) != cudaSuccess) cudaGetLastError();
     }
   cudaStream_t st = ws0->stream;
-  const size_t n = (size_t)p.n, hn = n + 1;
-  RQA_CUDA(grow(&ws0->gather, &ws0->gather_cap, (size_t)G * 4 * n + 2 * n), "allocating gather");
+  const size_t n = (size_t)p.n, hn = n + 1, hcount = 3 * hn + 2;
+  // gather area: [G][n] prefix, [G][n] suffix, [G][2n] column parts, [2n] row
+  // parts, then one histogram set (peer copy staging), 8-byte aligned
+  const size_t sum_words = (size_t)G * 4 * n + 2 * n;
+  const size_t hist_off = (sum_words + 1) & ~(size_t)1;
+  RQA_CUDA(grow(&ws0->gather, &ws0->gather_cap, hist_off + 2 * hcount), "allocating gather");
   int32_t* gpre = ws0->gather;
   int32_t* gsuf = gpre + (size_t)G * n;
   uint32_t* gcol = reinterpret_cast<uint32_t*>(gsuf + (size_t)G * n);
   uint32_t* grow_ = gcol + (size_t)G * 2 * n;
-  std::vector<int64_t> hsum(3 * hn + 2, 0), hpart(3 * hn + 2);
+  unsigned long long* stage = reinterpret_cast<unsigned long long*>(ws0->gather + hist_off);
+  unsigned long long* hsum = j0.hist;  // stripe 0's histograms accumulate the others
+  RQA_CUDA(cudaEventRecord(ws0->ev[3], st), "event");
+  const int hblocks = (int)std::min<size_t>((hcount + 255) / 256, 148 * 8);
   for (int g = 0; g < G; ++g) {
     const StripeJob& j = jobs[g];
     RQA_CUDA(cudaMemcpyPeerAsync(gpre + g * n, j0.dev, j.pre, j.dev, n * 4, st), "gather");
@@ -941,26 +993,21 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
       RQA_CUDA(cudaMemcpyPeerAsync(grow_ + 2 * j.lo, j0.dev, j.row + 2 * j.lo, j.dev,
                                    (size_t)(j.hi - j.lo) * 2 * 4, st),
                "gather");
-    RQA_CUDA(cudaSetDevice(j.dev), "cudaSetDevice");
-    RQA_CUDA(cudaMemcpy(hpart.data(), j.hist, (3 * hn + 2) * 8, cudaMemcpyDeviceToHost), "d2h");
-    RQA_CUDA(cudaSetDevice(j0.dev), "cudaSetDevice");
-    for (size_t q = 0; q < hsum.size(); ++q) hsum[q] += hpart[q];
+    if (g == 0) continue;
+    const unsigned long long* src = j.hist;
+    if (j.dev != j0.dev) {
+      RQA_CUDA(cudaMemcpyPeerAsync(stage, j0.dev, j.hist, j.dev, hcount * 8, st), "gather");
+      src = stage;
+    }
+    hist_accumulate_kernel<<<hblocks, 256, 0, st>>>(hsum, src, (int64_t)hcount);
+    RQA_CUDA(cudaGetLastError(), "launching histogram reduction");
+    g_launches++;
   }
-  // ws0->hist held stripe 0's partial histograms (copied above): reuse it
-  RQA_CUDA(cudaMemsetAsync(ws0->hist, 0, 3 * hn * sizeof(unsigned long long), st), "memset");
-  RQA_CUDA(cudaEventRecord(ws0->ev[3], st), "event");
-  rc = stitch_stripes(ws0, gpre, gsuf, gcol, grow_, bounds.data(), G, p.n, ws0->hist, st, err,
-                      errlen);
+  rc = stitch_stripes(ws0, gpre, gsuf, gcol, grow_, bounds.data(), G, p.n, hsum, st, err, errlen);
   if (rc) return rc;
   RQA_CUDA(cudaEventRecord(ws0->ev[4], st), "event");
-  RQA_CUDA(cudaMemcpyAsync(hpart.data(), ws0->hist, 3 * hn * 8, cudaMemcpyDeviceToHost, st), "d2h");
-  RQA_CUDA(cudaStreamSynchronize(st), "stitch");
-  for (size_t q = 0; q < 3 * hn; ++q) hsum[q] += hpart[q];
-  memcpy(diag, hsum.data(), hn * 8);
-  memcpy(vert, hsum.data() + hn, hn * 8);
-  memcpy(white, hsum.data() + 2 * hn, hn * 8);
-  *points = hsum[3 * hn];
-  if (mismatches) *mismatches = hsum[3 * hn + 1];
+  rc = copy_out(ws0, hsum, hn, flags, diag, vert, white, points, mismatches, st, err, errlen);
+  if (rc) return rc;
   if (timing) {
     float stitch_ms = 0.f, kern_ms = 0.f;
     cudaEventElapsedTime(&stitch_ms, ws0->ev[3], ws0->ev[4]);
@@ -972,9 +1019,11 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
     timing[2] = stitch_ms * 1e-3;
     timing[4] = wall;
     timing[5] = wall > 0 ? (double)p.n * (double)p.n / wall : 0.0;
-    timing[6] = 1024.0;
+    timing[6] = (double)j0.var.band_rows();
     timing[7] = (double)G;
-    timing[8] = precision == 32 ? 1.0 : -1.0;
+    timing[8] = j0.var.prec == 2 ? 2.0 : (double)j0.filt;
+    timing[9] = (double)j0.band32;
+    timing[10] = j0.cand;
   }
   return RQA_OK;
 }

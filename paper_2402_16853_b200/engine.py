@@ -100,9 +100,10 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         raise InvalidArgument("tile_size must be >= 1")  # engine.py:123-124
     if precision not in PRECISIONS:
         raise InvalidArgument(f"precision must be one of {sorted(PRECISIONS)}")
-    if (embedded.embedding_dimension != settings.embedding_dimension
-            or embedded.time_delay != settings.time_delay):
-        raise InvalidArgument("embedded series and settings disagree on m / tau")
+    # like the reference, the embedding parameters come from the embedded
+    # series (recurrence_block reads embedded.embedding_dimension / time_delay,
+    # embedding.py:137-143); settings' m / tau are not consulted here
+    m, tau = embedded.embedding_dimension, embedded.time_delay
     if devices is None:
         if device is not None:
             devices = [device]
@@ -123,8 +124,7 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
     mism = np.zeros(1, np.int64)
     tim = np.zeros(_native.TIMING_SLOTS, np.float64)
     p64 = ctypes.POINTER(ctypes.c_int64)
-    args = (s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0],
-            settings.embedding_dimension, settings.time_delay,
+    args = (s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), s.shape[0], m, tau,
             METRIC_CODES[settings.metric], float(settings.radius),
             settings.theiler_window, PRECISIONS[precision])
     outs = (diag.ctypes.data_as(p64), vert.ctypes.data_as(p64), white.ctypes.data_as(p64),
@@ -134,7 +134,7 @@ def run_analysis(embedded: EmbeddedSeries, settings: AnalysisSettings,
         _native.call("rqa_run_prec", *args, devices[0], FLAG_OUT_ZEROED, *outs)
     else:
         dv = (ctypes.c_int32 * len(devices))(*devices)
-        _native.call("rqa_run_multi", *args, dv, len(devices), *outs)
+        _native.call("rqa_run_multi", *args, dv, len(devices), FLAG_OUT_ZEROED, *outs)
     hist = LineHistograms(n, int(pts[0]), diag, vert, white)
     timing = {
         "create_recurrence_matrix": float(tim[1]),

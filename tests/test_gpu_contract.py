@@ -1,0 +1,116 @@
+"""Contract tests on the GPU: the documented drop-in binding and SPEC.md's
+acceptance criterion 3 (metric monotonicity)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gpu_available():
+    try:
+        from paper_2402_16853_b200 import _native
+
+        return _native.lib().rqa_device_count() > 0
+    except Exception:
+        return False
+
+
+if not _gpu_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2402_16853_b200 import (AnalysisSettings, LineHistograms, compute_measures,  # noqa: E402
+                                   embed, run_analysis)
+from paper_2402_16853_b200 import _native  # noqa: E402
+from paper_2402_16853_b200.engine import DEFAULT_TILE_SIZE, default_workers  # noqa: E402
+from paper_2402_16853_b200.errors import InvalidArgument, RQAError, SeriesTooShort  # noqa: E402
+
+
+def _integration_stub() -> str:
+    with open(os.path.join(REPO, "INTEGRATION.md")) as fh:
+        text = fh.read()
+    blocks = re.findall(r"```python\n(.*?)```", text, re.S)
+    stub = next(b for b in blocks if "def run_analysis" in b and "_lib.rqa_run" in b)
+    return stub
+
+
+def test_integration_stub_verbatim(oracle_lib):
+    """Execute INTEGRATION.md's ctypes binding exactly as written (only the
+    library path is made absolute) and compare it with the oracle.  The
+    timing buffer must hold RQA_TIMING_SLOTS doubles: a guard word after it
+    must survive the call."""
+    stub = _integration_stub()
+    assert "np.zeros(11)" in stub  # RQA_TIMING_SLOTS
+    assert _native.TIMING_SLOTS == 11
+    stub = stub.replace('ctypes.CDLL("librqa_b200.so")', f'ctypes.CDLL({_native.LIB_PATH!r})')
+    ns = {"DEFAULT_TILE_SIZE": DEFAULT_TILE_SIZE, "default_workers": default_workers,
+          "InvalidArgument": InvalidArgument, "SeriesTooShort": SeriesTooShort,
+          "RQAError": RQAError, "LineHistograms": LineHistograms}
+    exec(compile(stub, "INTEGRATION.md", "exec"), ns)
+    rng = np.random.default_rng(31)
+    for metric, m, tau, r, incl in (("l2", 3, 1, 0.15, True), ("linf", 2, 2, 0.1, False),
+                                    ("l1", 4, 1, 0.4, True)):
+        s = rng.uniform(0, 1, 2500)
+        st = AnalysisSettings(m, tau, metric, r, include_main_diagonal=incl)
+        h, timing = ns["run_analysis"](embed(s, m, tau), st)
+        want = oracle_lib.oracle_histograms(s, m, tau, metric, r, 0 if incl else 1,
+                                            tile_size=512)
+        assert h.recurrence_points == want[3]
+        assert np.array_equal(h.diagonal, want[0])
+        assert np.array_equal(h.vertical, want[1])
+        assert np.array_equal(h.white_vertical, want[2])
+        assert timing["total"] > 0
+    with pytest.raises(InvalidArgument):
+        ns["run_analysis"](embed(rng.uniform(0, 1, 100), 2, 1),
+                           AnalysisSettings(2, 1, "l2", 0.1), workers=0)
+
+
+def test_timing_buffer_bound():
+    """rqa_run writes exactly RQA_TIMING_SLOTS doubles."""
+    import ctypes
+
+    rng = np.random.default_rng(2)
+    s = rng.uniform(0, 1, 1000)
+    n = 999
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    pd = ctypes.POINTER(ctypes.c_double)
+    d, v, w = (np.zeros(n + 1, np.int64) for _ in range(3))
+    pts = np.zeros(1, np.int64)
+    tim = np.full(_native.TIMING_SLOTS + 4, -7.0)
+    _native.call("rqa_run", s.ctypes.data_as(pd), s.shape[0], 2, 1, 1, 0.1, 0, 0,
+                 d.ctypes.data_as(p64), v.ctypes.data_as(p64), w.ctypes.data_as(p64),
+                 pts.ctypes.data_as(p64), tim.ctypes.data_as(pd))
+    assert (tim[_native.TIMING_SLOTS:] == -7.0).all()
+
+
+def test_metric_monotonicity():
+    """SPEC.md:467 acceptance criterion 3: on >= 50 random cases with a fixed
+    radius, RR(Linf) >= RR(L2) >= RR(L1) (||x||_inf <= ||x||_2 <= ||x||_1)."""
+    rng = np.random.default_rng(467)
+    cases = 0
+    for i in range(60):
+        length = int(rng.integers(200, 3000))
+        m = int(rng.integers(1, 7))
+        tau = int(rng.integers(1, 4))
+        fam = i % 3
+        if fam == 0:
+            s = rng.uniform(0, 1, length)
+        elif fam == 1:
+            s = np.sin(np.linspace(0, 20 * np.pi, length)) + 0.2 * rng.normal(size=length)
+        else:
+            s = np.cumsum(rng.normal(size=length)) * 0.05
+        eps = float(rng.choice([0.05, 0.1, 0.3, 0.8]))
+        incl = bool(i % 2)
+        rr = {}
+        for metric in ("linf", "l2", "l1"):
+            st = AnalysisSettings(m, tau, metric, eps, include_main_diagonal=incl)
+            h, _ = run_analysis(embed(s, m, tau), st, device=0)
+            rr[metric] = compute_measures(h, st).rr
+        assert rr["linf"] >= rr["l2"] >= rr["l1"], (i, m, tau, eps, rr)
+        cases += 1
+    assert cases >= 50

@@ -194,7 +194,8 @@ def test_stripes_then_stitch_equal_single_run():
 
 
 def test_full_size_identities():
-    """C3 at full size (N = 2^20): conservation identities and symmetry-free checks."""
+    """C3 at full size (N = 2^20): conservation identities.
+    Bit-exact parity at this size is tests/test_gpu_full.py (full goldens)."""
     from paper_2402_16853_b200.workloads import WORKLOADS
 
     wl = WORKLOADS["C3"]
@@ -205,15 +206,6 @@ def test_full_size_identities():
     assert int((lengths * d).sum()) == p
     assert int((lengths * v).sum()) == p
     assert int((lengths * v).sum() + (lengths * w).sum()) == n * n
-    assert d[n] == 1                                      # main diagonal is one line
-    assert (d[1:n] % 2 == 0).all()                        # R = R^T pairs diagonals
-    # the prefix fixture is an exact sub-problem only for rows/cols < prefix;
-    # its recurrence rate must be close
-    fx = load_config("C3_65536") if "C3_65536" in config_tags() else None
-    if fx is not None:
-        rr_full = p / (n * n)
-        rr_pref = fx["result"]["recurrence_points"] / 65536 ** 2
-        assert abs(rr_full - rr_pref) < 2e-4
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 257, 1023, 1025])
