@@ -232,3 +232,27 @@ def test_fp32_stripes_then_stitch_equal_single_run():
         torch.cuda.synchronize()
         assert torch.equal(h, ref_h) and torch.equal(p, ref_p) and torch.equal(mm, ref_m), g
     assert int(ref_m.item()) > 0
+
+
+ENTROPIES = ("L_entr", "V_entr", "W_entr")
+
+
+@pytest.mark.parametrize("tag,length", [("C1", None), ("C2", None), ("C3", 65_538)])
+def test_fp32_mode_measures_relative_error(tag, length):
+    """north_star: fp32 mode reports its mismatched cells and its derived
+    measures against fp64 (measures.py:90-139).  On C1, C2 and the C3 prefix
+    every ratio measure (RR, DET, L, LAM, TT, W, DIV) is within 1e-6
+    relative and the maxima are equal; the entropies move more (a mismatched
+    cell shifts one count between two bins) and are within 1e-5.  Measured
+    on every workload by scripts/fp32_report.py (profiles/r02_fp32_report.json)."""
+    from paper_2402_16853_b200 import compare_precision
+    from paper_2402_16853_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS[tag]
+    rep = compare_precision(wl.series(length), wl.settings, device=0)
+    assert rep["mismatched_cells"] >= 0
+    for k, e in rep["rel_error"].items():
+        bound = 1e-5 if k in ENTROPIES else 1e-6
+        assert e <= bound, (tag, k, e, rep["mismatched_cells"])
+    for k in ("L_max", "V_max", "W_max"):
+        assert rep["measures_fp32"][k] == rep["measures_fp64"][k], k
