@@ -60,9 +60,9 @@ __host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot
   return ((top & 0xffffu) << 16) | (bot & 0xffffu);
 }
 
-// Candidate cells one warp resolves cooperatively per batch of two slots of a
-// 32-step chunk (sparse prefilter with large windows); more fall back to
-// per-lane resolution.  256 keeps two CTAs per SM.
+// Capacity (power of two) of a warp's streaming candidate list (prefilter
+// kernels): pending candidates plus one chunk's; a denser chunk is resolved
+// per lane.  256 keeps two CTAs per SM.
 constexpr int kCandCap = 256;
 
 struct SymSmem {
@@ -72,7 +72,7 @@ struct SymSmem {
   // esize 8: float64 row/column windows; 4: float32 windows (f32 filter
   // kernels), the row window stored as R/2 interleaved slot pairs of
   // HS + W + 4 float2 each (rqa_unit.cuh, packed f32x2 evaluation).
-  // coop: per-warp candidate list + result words (prefilter, large windows)
+  // coop: per-warp streaming candidate list (prefilter kernels)
   __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, bool coop = false) {
     D = 32 * NW;
     HS = D;
@@ -98,7 +98,7 @@ struct SymSmem {
     // bins, two mbarriers (16 B), the dummy bin of hist_red (16 B reserved)
     off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
     off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
-    total = off_cres + (coop ? (size_t)NW * R * 32 * sizeof(uint32_t) : 0);
+    total = off_cres;
   }
 };
 

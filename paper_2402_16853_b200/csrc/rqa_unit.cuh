@@ -105,11 +105,11 @@ __device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int
   return make_uint2(w64, w32);
 }
 
-// Prefilter candidates are resolved warp-cooperatively (32 at a time from a
-// shared list) when a candidate's exact sum is long (m >= 5); for short sums
-// the per-lane loop is cheaper than building the list.
+// Prefilter kernels (PREC 2) resolve their candidates warp-cooperatively from
+// a per-warp list that streams across the chunks of an iteration: every
+// round takes 32 candidates at full SIMD width (rqa_unit.cuh, phase 1).
 template <int PREC, int M>
-constexpr bool kCoopResolve = (PREC == 2) && (M >= 5);
+constexpr bool kCoopResolve = (PREC == 2);
 
 template <int METRIC, int M, int TAU, int NW, int R, int MINB, int PREC = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
@@ -321,6 +321,179 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       if (__all_sync(0xffffffffu, kdr[r] >= 0 && kdr[r] < nrem && lastc[r] == HS))
         fullmask |= 1u << r;
 
+    // word (slot r, chunk c) is final: diagonal runs of its 32 rows, then its
+    // transposed row word goes to rowbuf
+    auto finish_word = [&](int r, int c, uint32_t word) {
+      const int kd = kdr[r];
+      if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
+      if (!warm && !(skip & 1) && ((fullmask >> r) & 1u)) {
+        runs_pass(word, 32, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
+      } else if (!warm && !(skip & 1)) {
+        const bool live = kd >= 0 && kd < nrem;
+        const int rel = lastc[r] - 32 * c;
+        runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
+                  lane);
+        if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+          // the segment is cut by the matrix's right edge inside the slot
+          diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
+                      LineSink{&hist, kd == 0 ? 1u : 2u});
+          st[r] = RunState{1u, 0u};
+        }
+      }
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
+                   "r"(tr(word))
+                   : "memory");
+    };
+
+    if constexpr (kPre) {
+      // ---- phase 1: candidate words (AND of the m shifted predicates
+      // |d| <= D*) of every chunk go to this lane's rowbuf slots; their set
+      // bits are appended to the warp's candidate list, which is resolved 32
+      // at a time (exact float64 sums in the reference's order) as soon as
+      // a full round is queued.  A failing candidate clears its bit.
+      static_assert(R <= 4 && NCH <= 8, "candidate encoding: 2-bit slot, 3-bit chunk");
+      uint16_t* cl = reinterpret_cast<uint16_t*>(smem + L.off_cand) + wv * kCandCap;
+      const uint32_t wbase = smem_u32(rowbuf + wv * H);  // this warp's rowbuf words
+      auto resolve_round = [&](uint32_t head, uint32_t avail) {
+        if ((uint32_t)lane < avail) {
+          const uint32_t e = cl[(head + (uint32_t)lane) & (uint32_t)(kCandCap - 1)];
+          const int r = (int)(e >> 13), ce = (int)((e >> 10) & 7u), sl = (int)((e >> 5) & 31u),
+                    t = (int)(e & 31u);
+          const int off = r * HS + 32 * ce;
+          if (!pre_exact(s_row + off + t, s_col - lane + sl + 32 * ce + t)) {
+            const uint32_t addr = wbase + 4u * (uint32_t)(off + sl);
+            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(~(1u << t)) : "memory");
+          }
+        }
+      };
+      uint32_t lhead = 0u, ltail = 0u;  // warp-uniform list cursors
+      // short sums (m <= 4): the list holds nonzero candidate WORDS (slot,
+      // chunk, lane); the lane that takes an entry resolves every candidate
+      // of that word and rewrites it (it is the word's only writer until
+      // phase 2).  Cheaper to build than a per-cell list at the sparse
+      // candidate densities where the prefilter is chosen.
+      constexpr bool kWordList = (M <= 4);
+      auto resolve_words = [&](uint32_t head, uint32_t avail) {
+        if ((uint32_t)lane < avail) {
+          const uint32_t e = cl[(head + (uint32_t)lane) & (uint32_t)(kCandCap - 1)];
+          const int r = (int)(e >> 8), ce = (int)((e >> 5) & 7u), sl = (int)(e & 31u);
+          const int off = r * HS + 32 * ce;
+          const uint32_t addr = wbase + 4u * (uint32_t)(off + sl);
+          uint32_t cand = lds_u32(addr), res = cand;
+          const F* rp = s_row + off;
+          const F* cp = s_col - lane + sl + 32 * ce;
+          while (cand) {
+            const int t = __ffs(cand) - 1;
+            cand &= cand - 1u;
+            if (!pre_exact(rp + t, cp + t)) res &= ~(1u << t);
+          }
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(res) : "memory");
+        }
+      };
+      for (int c = 0; c < NCH; ++c) {
+        const F* colc = s_col + 32 * c;
+        const F* rowc = s_row + 32 * c;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const double cv = colc[t + kW];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double d = __dsub_rn(rowc[r * HS + t + kW], cv);
+            if (fabs(d) <= athr) ph[r][(t + kW) >> 5] |= 1u << ((t + kW) & 31);
+          }
+        }
+        uint32_t wr[R];
+        int kc = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t w = ph[r][0];
+#pragma unroll
+          for (int k = 1; k < M; ++k)
+            w &= __funnelshift_rc(ph[r][(k * TAU) >> 5], ph[r][((k * TAU) >> 5) + 1],
+                                  (k * TAU) & 31);
+#pragma unroll
+          for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
+          ph[r][NPH - 1] = 0u;
+          w = kdr[r] < theiler ? 0u : w;  // Theiler-excluded cells need no sum
+          wr[r] = w;
+          kc += __popc(w);
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
+                       "r"(w)
+                       : "memory");
+        }
+        if constexpr (kWordList) {
+          // at most R * 32 new entries per chunk: the list never overflows
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint32_t mk = __ballot_sync(0xffffffffu, wr[r] != 0u);
+            if (wr[r] != 0u)
+              cl[(ltail + __popc(mk & evq.lt_mask)) & (uint32_t)(kCandCap - 1)] =
+                  (uint16_t)((r << 8) | (c << 5) | lane);
+            ltail += __popc(mk);
+          }
+          __syncwarp();
+          while (ltail - lhead >= 32u) {
+            resolve_words(lhead, 32u);
+            lhead += 32u;
+          }
+          continue;
+        }
+        int incl = kc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t tot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+        if (ltail - lhead + tot <= (uint32_t)kCandCap) {
+          uint32_t pos = ltail + (uint32_t)(incl - kc);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            uint32_t w = wr[r];
+            while (w) {
+              const int t = __ffs(w) - 1;
+              w &= w - 1u;
+              cl[pos++ & (uint32_t)(kCandCap - 1)] =
+                  (uint16_t)((r << 13) | (c << 10) | (lane << 5) | t);
+            }
+          }
+          ltail += tot;
+          __syncwarp();
+          while (ltail - lhead >= 32u) {
+            resolve_round(lhead, 32u);
+            lhead += 32u;
+          }
+        } else {
+          // dense chunk: every lane resolves its own candidates
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            uint32_t cand = wr[r], res = wr[r];
+            while (cand) {
+              const int t = __ffs(cand) - 1;
+              cand &= cand - 1u;
+              if (!pre_exact(rowc + r * HS + t, colc + t)) res &= ~(1u << t);
+            }
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
+                         "r"(res)
+                         : "memory");
+          }
+        }
+      }
+      __syncwarp();
+      while (ltail != lhead) {  // the last, partial round
+        const uint32_t avail = min(ltail - lhead, 32u);
+        if constexpr (kWordList) resolve_words(lhead, avail);
+        else resolve_round(lhead, avail);
+        lhead += avail;
+      }
+      __syncwarp();
+      // ---- phase 2: final words -> diagonal runs, transposed row words
+      for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          finish_word(r, c, lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)));
+      }
+    } else
     for (int c = 0; c < NCH; ++c) {
       uint32_t dw[R];
       float amb[R];  // f32 filter: min |acc32 - c32| over the word (per pair when packed)
@@ -456,80 +629,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
         }
       }
-      if constexpr (kCoopResolve<PREC, M>) {
-        // candidate words of every slot, then the exact sums 32 candidates at
-        // a time from a per-warp list (full SIMD width), results ORed back
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          uint32_t w = ph[r][0];
-#pragma unroll
-          for (int k = 1; k < M; ++k)
-            w &= __funnelshift_rc(ph[r][(k * TAU) >> 5], ph[r][((k * TAU) >> 5) + 1],
-                                  (k * TAU) & 31);
-#pragma unroll
-          for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
-          ph[r][NPH - 1] = 0u;
-          dw[r] = kdr[r] < theiler ? 0u : w;  // Theiler-excluded cells need no sum
-        }
-        constexpr int RB = (R >= 2) ? 2 : 1;  // slots per cooperative batch
-        uint16_t* cl = reinterpret_cast<uint16_t*>(smem + L.off_cand) + wv * kCandCap;
-        uint32_t* cres = reinterpret_cast<uint32_t*>(smem + L.off_cres) + wv * R * 32;
-#pragma unroll
-        for (int r0 = 0; r0 < R; r0 += RB) {
-          int kc = 0;
-#pragma unroll
-          for (int r = r0; r < r0 + RB; ++r) kc += __popc(dw[r]);
-          const int K = (int)__reduce_add_sync(0xffffffffu, (unsigned)kc);
-          if (K > 0 && K <= kCandCap) {
-            int incl = kc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += y;
-            }
-            int pos = incl - kc;
-#pragma unroll
-            for (int r = r0; r < r0 + RB; ++r) {
-              uint32_t w = dw[r];
-              while (w) {
-                const int t = __ffs(w) - 1;
-                w &= w - 1u;
-                cl[pos++] = (uint16_t)((r << 10) | (lane << 5) | t);
-              }
-              cres[r * 32 + lane] = 0u;
-            }
-            __syncwarp();
-            for (int base = 0; base < K; base += 32) {
-              const int idx = base + lane;
-              if (idx < K) {
-                const uint32_t e = cl[idx];
-                const int r = (int)(e >> 10), sl = (int)((e >> 5) & 31u), t = (int)(e & 31u);
-                if (pre_exact(rowc + r * HS + t, colc - lane + sl + t))
-                  atomicOr(&cres[r * 32 + sl], 1u << t);
-              }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int r = r0; r < r0 + RB; ++r) dw[r] = cres[r * 32 + lane];
-            __syncwarp();
-          } else if (K > 0) {  // very dense: every lane resolves its own cells
-#pragma unroll
-            for (int r = r0; r < r0 + RB; ++r) {
-              uint32_t cand = dw[r], res = 0u;
-              while (cand) {
-                const int t = __ffs(cand) - 1;
-                cand &= cand - 1u;
-                if (pre_exact(rowc + r * HS + t, colc + t)) res |= 1u << t;
-              }
-              dw[r] = res;
-            }
-          }
-        }
-      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         uint32_t word;
-        if constexpr (kAnd && !kCoopResolve<PREC, M>) {
+        if constexpr (kAnd) {  // L-inf: AND of the m shifted per-component predicates
           word = ph[r][0];
 #pragma unroll
           for (int k = 1; k < M; ++k)
@@ -538,38 +641,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
           for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
           ph[r][NPH - 1] = 0u;
-          if constexpr (kPre && !kCoopResolve<PREC, M>) {
-            // exact sums (reference order) for the candidate cells only
-            uint32_t cand = kdr[r] < theiler ? 0u : word, res = 0u;
-            while (cand) {
-              const int t = __ffs(cand) - 1;
-              cand &= cand - 1u;
-              if (pre_exact(rowc + r * HS + t, colc + t)) res |= 1u << t;
-            }
-            word = res;
-          }
         } else {
           word = dw[r];
         }
-        const int kd = kdr[r];
-        if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-        if (!warm && !(skip & 1) && ((fullmask >> r) & 1u)) {
-          runs_pass(word, 32, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
-        } else if (!warm && !(skip & 1)) {
-          const bool live = kd >= 0 && kd < nrem;
-          const int rel = lastc[r] - 32 * c;
-          runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
-                    lane);
-          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
-            // the segment is cut by the matrix's right edge inside the slot
-            diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
-                        LineSink{&hist, kd == 0 ? 1u : 2u});
-            st[r] = RunState{1u, 0u};
-          }
-        }
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
-                     "r"(tr(word))
-                     : "memory");
+        finish_word(r, c, word);
       }
     }
     __syncthreads();
