@@ -225,8 +225,7 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
       "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(q.ring_sa + 16u * slot),
       "r"(bnd), "r"(cur), "r"((diag_weight << 1) | (mkfirst ? 1u : 0u)), "r"(0u),
-      "r"(ev ? 1u : 0u)
-      : "memory");
+      "r"(ev ? 1u : 0u));  // no memory clobber: the ring is only accessed through asm
   q.tail += __popc(m);
 }
 

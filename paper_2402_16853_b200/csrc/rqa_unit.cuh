@@ -321,28 +321,39 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       if (__all_sync(0xffffffffu, kdr[r] >= 0 && kdr[r] < nrem && lastc[r] == HS))
         fullmask |= 1u << r;
 
-    // word (slot r, chunk c) is final: diagonal runs of its 32 rows, then its
-    // transposed row word goes to rowbuf
-    auto finish_word = [&](int r, int c, uint32_t word) {
-      const int kd = kdr[r];
-      if (kd < theiler) word = 0u;  // also the lower triangle kd < 0
-      if (!warm && !(skip & 1) && ((fullmask >> r) & 1u)) {
-        runs_pass(word, 32, st[r], kd == 0 ? 1u : 2u, evq, hist, lane);
-      } else if (!warm && !(skip & 1)) {
-        const bool live = kd >= 0 && kd < nrem;
-        const int rel = lastc[r] - 32 * c;
-        runs_pass(word, live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq, hist,
-                  lane);
-        if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
-          // the segment is cut by the matrix's right edge inside the slot
-          diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
-                      LineSink{&hist, kd == 0 ? 1u : 2u});
-          st[r] = RunState{1u, 0u};
-        }
+    // the R words of chunk c are final: their transposed row words go to
+    // rowbuf (the R transposes are independent and interleave), then the
+    // diagonal runs of their 32 rows; the event ring is drained after every
+    // second slot (<= 63 queued + 2 x 32 pushed < kQueueCap)
+    auto finish_chunk = [&](int c, uint32_t (&w)[R]) {
+      uint32_t tw[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (kdr[r] < theiler) w[r] = 0u;  // also the lower triangle kd < 0
+        tw[r] = tr(w[r]);
       }
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
-                   "r"(tr(word))
-                   : "memory");
+#pragma unroll
+      for (int r = 0; r < R; ++r) rowbuf[wv * H + r * HS + 32 * c + lane] = tw[r];
+      if (warm || (skip & 1)) return;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int kd = kdr[r];
+        if ((fullmask >> r) & 1u) {
+          runs_push(w[r], 32, st[r], kd == 0 ? 1u : 2u, evq);
+        } else {
+          const bool live = kd >= 0 && kd < nrem;
+          const int rel = lastc[r] - 32 * c;
+          runs_push(w[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq);
+          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
+            // the segment is cut by the matrix's right edge inside the slot
+            diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
+                        LineSink{&hist, kd == 0 ? 1u : 2u});
+            st[r] = RunState{1u, 0u};
+          }
+        }
+        if ((r & 1) || r == R - 1)
+          if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+      }
     };
 
     if constexpr (kPre) {
@@ -489,9 +500,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       __syncwarp();
       // ---- phase 2: final words -> diagonal runs, transposed row words
       for (int c = 0; c < NCH; ++c) {
+        uint32_t w[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          finish_word(r, c, lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)));
+        for (int r = 0; r < R; ++r) w[r] = lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c));
+        finish_chunk(c, w);
       }
     } else
     for (int c = 0; c < NCH; ++c) {
@@ -629,11 +641,11 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
         }
       }
+      uint32_t words[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        uint32_t word;
         if constexpr (kAnd) {  // L-inf: AND of the m shifted per-component predicates
-          word = ph[r][0];
+          uint32_t word = ph[r][0];
 #pragma unroll
           for (int k = 1; k < M; ++k)
             word &= __funnelshift_rc(ph[r][(k * TAU) >> 5], ph[r][((k * TAU) >> 5) + 1],
@@ -641,11 +653,12 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 #pragma unroll
           for (int q = 0; q + 1 < NPH; ++q) ph[r][q] = ph[r][q + 1];
           ph[r][NPH - 1] = 0u;
+          words[r] = word;
         } else {
-          word = dw[r];
+          words[r] = dw[r];
         }
-        finish_word(r, c, word);
       }
+      finish_chunk(c, words);
     }
     __syncthreads();
 
@@ -735,17 +748,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         if (!(skip & 4) && x >= rs_[PR - 1]) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
           // shifted into aligned columns, transposed, met bottom-up
-          // 32-bit shared addresses of the row words (rowbuf / previous iteration)
-          uint32_t rb_sa = smem_u32(rowbuf), pv_sa = smem_u32(prev_cur);
-          asm volatile("" : "+r"(rb_sa), "+r"(pv_sa));  // keep in registers (no re-derivation)
           auto col_step = [&](int c, const int* lim, auto full) {
             const int wp = (wv - c) & (NW - 1);
 #pragma unroll
             for (int p = 0; p < PR; ++p) {
               const int lrow = rs_[p] * HS + 32 * c + lane;
-              const uint32_t w1 = lds_u32(rb_sa + 4u * (uint32_t)(wp * H + lrow));
-              const uint32_t w0 = lds_u32(wp > 0 ? rb_sa + 4u * (uint32_t)((wp - 1) * H + lrow)
-                                                 : pv_sa + 4u * (uint32_t)lrow);
+              const uint32_t w1 = rowbuf[wp * H + lrow];
+              const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
               const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
               if constexpr (decltype(full)::value) {  // every lane: 32 rows of the column
                 runs_push(__brev(colw), 32, cur[p], 0u, evq);
