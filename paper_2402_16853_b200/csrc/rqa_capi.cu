@@ -94,7 +94,9 @@ struct Workspace {
   size_t s_cap = 0;  // elements
   float* sf_pad = nullptr;     // f32 filter: samples rounded to float32
   size_t sf_cap = 0;
-  unsigned long long* maxbits = nullptr;  // max |s| as float64 bits (NaN/inf: >= 0x7ff0...)
+  unsigned long long* maxbits = nullptr;  // [1]: prefilter sampling hit counter
+  unsigned long long* stats = nullptr;    // [2]: max finite |s| (float64 bits), non-finite flag
+  size_t stats_cap = 0;
   uint16_t* ps = nullptr;      // P and S (compact band layout)
   size_t ps_cap = 0;  // elements
   uint32_t* cs = nullptr;      // column-part summaries (compact band layout)
@@ -166,6 +168,7 @@ struct Problem {
   unsigned long long* mism = nullptr;
   double dstar = 0.0;   // prefilter bound (var.prec == 2)
   double cand = -1.0;   // sampled prefilter candidate fraction (-1: not sampled)
+  float pre_negd2 = 0.f;  // -D2 of the packed float32 prefilter predicate
 };
 
 int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
@@ -288,22 +291,30 @@ __global__ void hist_accumulate_kernel(unsigned long long* __restrict__ dst,
   }
 }
 
+// float32 copy of the series; out[0] = max |s| over the finite samples (as
+// float64 bits), out[1] = 1 if any sample is NaN or infinite.
 __global__ void prep_f32_kernel(const double* __restrict__ s, float* __restrict__ sf, int64_t count,
-                                unsigned long long* maxbits) {
+                                unsigned long long* out) {
   unsigned long long mx = 0;
+  bool nonfinite = false;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < count;
        q += (int64_t)gridDim.x * blockDim.x) {
     const double x = s[q];
     sf[q] = __double2float_rn(x);
     const unsigned long long b = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
-    mx = b > mx ? b : mx;
+    if (b >= 0x7ff0000000000000ull) nonfinite = true;
+    else mx = b > mx ? b : mx;
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
     const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = y > mx ? y : mx;
   }
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxbits, mx);
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  if ((threadIdx.x & 31) == 0) {
+    if (mx) atomicMax(out, mx);
+    if (nonfinite) atomicOr(out + 1, 1ull);
+  }
 }
 
 int cuda_fail(cudaError_t e, const char* what, char* err, size_t errlen) {
@@ -330,6 +341,50 @@ int stage_series(Workspace* ws, const Problem& p, const double* src, cudaMemcpyK
   return RQA_OK;
 }
 
+// float32 copy of the staged series (same padding) plus max |s| and whether
+// every sample is finite; sets p->sf.  One small kernel + a 8-byte readback.
+int stage_f32(Workspace* ws, Problem* p, cudaStream_t st, double* maxabs, bool* finite, char* err,
+              size_t errlen) {
+  const size_t count = (size_t)(p->len + 2 * p->pad);
+  RQA_CUDA(grow(&ws->sf_pad, &ws->sf_cap, count), "allocating float32 series");
+  RQA_CUDA(grow(&ws->stats, &ws->stats_cap, 2), "allocating");
+  RQA_CUDA(cudaMemsetAsync(ws->stats, 0, 2 * sizeof(unsigned long long), st), "memset");
+  prep_f32_kernel<<<148 * 4, 256, 0, st>>>(ws->s_pad, ws->sf_pad, (int64_t)count, ws->stats);
+  RQA_CUDA(cudaGetLastError(), "launching f32 staging");
+  g_launches++;
+  unsigned long long mb[2] = {0, 0};
+  RQA_CUDA(cudaMemcpyAsync(mb, ws->stats, sizeof mb, cudaMemcpyDeviceToHost, st), "d2h");
+  RQA_CUDA(cudaStreamSynchronize(st), "f32 staging");
+  *finite = mb[1] == 0;
+  memcpy(maxabs, &mb[0], sizeof *maxabs);
+  p->sf = ws->sf_pad + p->pad;
+  return RQA_OK;
+}
+
+// Bound of the packed float32 prefilter predicate (kF32Pred kernels): with
+// u = 2^-24 and M = max |s|, |d64| <= D* implies
+//   |fl32(fl32(r) - fl32(c))| <= B = D* (1 + 2^-50) + u (2M + D*) (1 + 2^-20),
+// so every component candidate of the float64 prefilter has d32^2 < D2 for
+// the float D2 > B^2 returned here (fma(d32, d32, -D2) is then negative, its
+// sign bit set).  NaN / infinite samples need no bound: every cell with such
+// a component is non-recurrent in the reference (NaN or infinite sum), and
+// whatever the float32 predicate says about it, the exact float64 sum of a
+// candidate decides.  Returns false when the finite samples or the bound are
+// out of range (|s| >= 1e30 would overflow float32): no prefilter then.
+bool prefilter_f32_bound(double dstar, double maxabs, float* d2) {
+  if (!(maxabs < 1e30) || !(dstar >= 0) || !(dstar < 1e18)) return false;
+  const double u = std::ldexp(1.0, -24);
+  const double B = dstar * (1.0 + std::ldexp(1.0, -50)) +
+                   u * (2.0 * maxabs + dstar) * (1.0 + std::ldexp(1.0, -20)) +
+                   4.0 * u * u * maxabs;
+  const double B2 = B * B * (1.0 + std::ldexp(1.0, -40));
+  if (!(B2 < 1e37)) return false;
+  float f = (float)B2;
+  if ((double)f < B2) f = std::nextafter(f, INFINITY);
+  *d2 = std::nextafter(f, INFINITY);  // strictly above B^2
+  return true;
+}
+
 // Precision plan after the series is staged: precision 32 always runs the f32
 // kernels (fp32 mode).  Precision 64 runs the float64 kernels by default: the
 // f32 filter issues 8 % fewer instructions on C3 but moves the evaluation
@@ -345,20 +400,10 @@ int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
   Variant fv;
   const bool packed = find_variant_f32(p->metric, p->m, p->tau, true, &fv);
   if (p->precision == 64 && (want == 0 || !packed)) return RQA_OK;
-  const size_t count = (size_t)(p->len + 2 * p->pad);
-  RQA_CUDA(grow(&ws->sf_pad, &ws->sf_cap, count), "allocating float32 series");
-  RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 1), "allocating");
-  RQA_CUDA(cudaMemsetAsync(ws->maxbits, 0, sizeof(unsigned long long), st), "memset");
-  prep_f32_kernel<<<148 * 4, 256, 0, st>>>(ws->s_pad, ws->sf_pad, (int64_t)count, ws->maxbits);
-  RQA_CUDA(cudaGetLastError(), "launching f32 staging");
-  g_launches++;
-  unsigned long long mb = 0;
-  RQA_CUDA(cudaMemcpyAsync(&mb, ws->maxbits, sizeof mb, cudaMemcpyDeviceToHost, st), "d2h");
-  RQA_CUDA(cudaStreamSynchronize(st), "f32 staging");
-  const bool finite = mb < 0x7ff0000000000000ull;
-  double maxabs;
-  memcpy(&maxabs, &mb, sizeof maxabs);
-  p->sf = ws->sf_pad + p->pad;
+  double maxabs = 0.0;
+  bool finite = false;
+  int rc = stage_f32(ws, p, st, &maxabs, &finite, err, errlen);
+  if (rc) return rc;
   if (p->precision == 32) {
     const float t32 = threshold_for32(p->metric, p->m, p->radius);
     p->thr32 = t32;
@@ -418,6 +463,16 @@ int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
     RQA_CUDA(cudaStreamSynchronize(st), "candidate sampling");
     p->cand = (double)hits / samples;
     if (p->cand > prefilter_max(p->m)) return RQA_OK;
+  }
+  if (pv.f32pred) {
+    double maxabs = 0.0;
+    bool finite = false;
+    int rc = stage_f32(ws, p, st, &maxabs, &finite, err, errlen);
+    if (rc) return rc;
+    float d2 = 0.f;
+    (void)finite;
+    if (!prefilter_f32_bound(dstar, maxabs, &d2)) return RQA_OK;
+    p->pre_negd2 = -d2;
   }
   p->dstar = dstar;
   p->var = pv;
@@ -554,6 +609,7 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.all_amb = p.all_amb;
   a.mism = p.mism;
   a.dstar = p.dstar;
+  a.pre_negd2 = p.pre_negd2;
   ua.units = ws->units;
   ua.rowpiece = ws->rowpiece;
   RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
@@ -1164,6 +1220,7 @@ int rqa_release(void) {
     cudaFree(ws->s_pad);
     cudaFree(ws->sf_pad);
     cudaFree(ws->maxbits);
+    cudaFree(ws->stats);
     cudaFree(ws->ps);
     cudaFree(ws->cs);
     cudaFree(ws->rowlead);

@@ -47,6 +47,10 @@ struct SymArgs {
   int all_amb;               // 1: every word is re-evaluated (band not certifiable)
   unsigned long long* mism;  // fp32 mode: cells whose fp32 and fp64 decisions differ
   double dstar;              // prefilter (PREC 2): |d| <= dstar for every term of a candidate
+  // packed float32 prefilter predicate (PREC 2, m <= 4): a cell is a
+  // component candidate iff fma(d32, d32, pre_negd2) < 0 (sign bit), a
+  // certified superset of |d| <= dstar (rqa_capi.cu plan_prefilter)
+  float pre_negd2;
 };
 
 // Compact per-band offset of entries kd (or c - i0) in [0, n - i0).
@@ -68,12 +72,17 @@ constexpr int kCandCap = 256;
 struct SymSmem {
   int H, HS, D, W, CW;
   size_t off_row, off_col0, off_col1, off_rowbuf, off_prev, off_colst, off_rowst, off_queue,
-      off_hist, off_cand, off_cres, total;
+      off_hist, off_cand, off_cres, off_rowf, off_colf0, off_colf1, total;
+  int CWF;  // float32 column window (f32pred)
   // esize 8: float64 row/column windows; 4: float32 windows (f32 filter
   // kernels), the row window stored as R/2 interleaved slot pairs of
   // HS + W + 4 float2 each (rqa_unit.cuh, packed f32x2 evaluation).
   // coop: per-warp streaming candidate list (prefilter kernels)
-  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, bool coop = false) {
+  // f32pred: float32 copies of the windows for the packed prefilter
+  // predicate (row window as R/2 slot pairs of HS + W + 4 float2, two float
+  // column buffers), appended at the end
+  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, bool coop = false,
+                              bool f32pred = false) {
     D = 32 * NW;
     HS = D;
     H = R * HS;
@@ -99,6 +108,14 @@ struct SymSmem {
     off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
     off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
     total = off_cres;
+    CWF = ((HS + D + W + 4) + 3) & ~3;
+    off_rowf = off_colf0 = off_colf1 = total;
+    if (f32pred) {
+      off_rowf = (total + 15) & ~(size_t)15;
+      off_colf0 = (off_rowf + (size_t)(R / 2) * (HS + W + 4) * sizeof(float2) + 15) & ~(size_t)15;
+      off_colf1 = off_colf0 + (size_t)CWF * sizeof(float);
+      total = off_colf1 + (size_t)CWF * sizeof(float);
+    }
   }
 };
 

@@ -110,6 +110,14 @@ __device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int
 // round takes 32 candidates at full SIMD width (rqa_unit.cuh, phase 1).
 template <int PREC, int M>
 constexpr bool kCoopResolve = (PREC == 2);
+// Short-window prefilter kernels evaluate the per-component predicate in
+// packed float32 (sub/fma.rn.f32x2 over slot pairs, the sign bit of
+// d32*d32 - D32^2 funnel-shifted into the word): 2.5 instructions per cell
+// instead of DADD + DSETP + LOP.  It is a certified superset of the float64
+// predicate |d| <= D* (rqa_capi.cu plan_prefilter), and every candidate is
+// still decided by the exact float64 sum, so the result is unchanged.
+template <int PREC, int M, int R>
+constexpr bool kF32Pred = (PREC == 2) && (M >= 2) && (M <= 4) && (R % 2 == 0);
 
 template <int METRIC, int M, int TAU, int NW, int R, int MINB, int PREC = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
@@ -141,7 +149,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   using F = typename std::conditional<kF32, float, double>::type;
   constexpr int RP = (R + 1) / 2;  // slot pairs
   const int W = kDirect ? W_rt : kW;
-  const SymSmem L(NW, R, W, (int)sizeof(F), kCoopResolve<PREC, M>);
+  constexpr bool kFP = kF32Pred<PREC, M, R>;
+  const SymSmem L(NW, R, W, (int)sizeof(F), kCoopResolve<PREC, M>, kFP);
   const int PS = HS + W + 4;       // packed row window: float2 elements per slot pair
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -214,6 +223,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   } else {
     for (int q = tid; q < H + W; q += NW * 32) s_row[q] = gs[i0 + q];
   }
+  if constexpr (kFP) {
+    float2* rowf = reinterpret_cast<float2*>(smem + L.off_rowf);
+    for (int q = tid; q < (R / 2) * (HS + W); q += NW * 32) {
+      const int pr = q / (HS + W), u = q - pr * (HS + W);
+      rowf[pr * (HS + W + 4) + u] = make_float2(a.sf[i0 + 2 * pr * HS + u], a.sf[i0 + (2 * pr + 1) * HS + u]);
+    }
+  }
   for (int q = tid; q < 2 * H; q += NW * 32) prevbuf[q] = 0u;
   for (int q = tid; q < NW * R * 32; q += NW * 32) colst[q] = make_uint2(0u, 0u);
   for (int q = tid; q < R * D; q += NW * 32) rowst[q] = make_uint2(0u, 0u);
@@ -224,11 +240,17 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   }
   __syncthreads();
   const uint32_t col_bytes = (uint32_t)(L.CW * sizeof(F));
+  const uint32_t colf_bytes = kFP ? (uint32_t)(L.CWF * sizeof(float)) : 0u;
   if (tid == 0) {
     const F* src;
     col_window_src(gs, i0 + (int64_t)xfirst * D, &src);
-    mbar_expect_tx_arrive(&bar[0], col_bytes);
+    mbar_expect_tx_arrive(&bar[0], col_bytes + colf_bytes);
     tma_load_1d(smem + L.off_col0, src, col_bytes, &bar[0]);
+    if constexpr (kFP) {
+      const float* srcf;
+      col_window_src(a.sf, i0 + (int64_t)xfirst * D, &srcf);
+      tma_load_1d(smem + L.off_colf0, srcf, colf_bytes, &bar[0]);
+    }
   }
 
   RunState st[R];  // diagonal run state of the current (band, slot) segment
@@ -253,8 +275,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     if (tid == 0 && x + 1 < xb) {
       const F* src;
       col_window_src(gs, i0 + kx + D, &src);
-      mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes);
+      mbar_expect_tx_arrive(&bar[buf ^ 1], col_bytes + colf_bytes);
       tma_load_1d(smem + (buf ? L.off_col0 : L.off_col1), src, col_bytes, &bar[buf ^ 1]);
+      if constexpr (kFP) {
+        const float* srcf;
+        col_window_src(a.sf, i0 + kx + D, &srcf);
+        tma_load_1d(smem + (buf ? L.off_colf0 : L.off_colf1), srcf, colf_bytes, &bar[buf ^ 1]);
+      }
     }
     mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
     const int co = (int)((((uintptr_t)(gs + i0 + kx)) & 15u) / sizeof(F));
@@ -404,13 +431,48 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       for (int c = 0; c < NCH; ++c) {
         const F* colc = s_col + 32 * c;
         const F* rowc = s_row + 32 * c;
+        if constexpr (kFP) {
+          // packed float32 predicate over slot pairs; bit of step t enters
+          // at bit 0 and ends at bit 31 - t (reversed after the chunk)
+          const float* colf =
+              reinterpret_cast<const float*>(smem + (buf ? L.off_colf1 : L.off_colf0)) +
+              (int)((((uintptr_t)(a.sf + i0 + kx)) & 15u) / sizeof(float)) + delta + 32 * c;
+          const unsigned long long* rowf =
+              reinterpret_cast<const unsigned long long*>(smem + L.off_rowf) + 32 * c;
+          const unsigned long long nd2 = f2_pack(a.pre_negd2, a.pre_negd2);
+          uint32_t nw[R];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const double cv = colc[t + kW];
+          for (int r = 0; r < R; ++r) nw[r] = 0u;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const float cv = colf[t + kW];
+            const unsigned long long cc = f2_pack(cv, cv);
+#pragma unroll
+            for (int pr = 0; pr < R / 2; ++pr) {
+              const unsigned long long rv = rowf[pr * (HS + W + 4) + t + kW];
+              unsigned long long d, x;
+              asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(rv), "l"(cc));
+              asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(x) : "l"(d), "l"(nd2));
+              nw[2 * pr] = __funnelshift_l((uint32_t)x, nw[2 * pr], 1);
+              nw[2 * pr + 1] = __funnelshift_l((uint32_t)(x >> 32), nw[2 * pr + 1], 1);
+            }
+          }
+          constexpr int q0 = kW >> 5, sh = kW & 31;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const double d = __dsub_rn(rowc[r * HS + t + kW], cv);
-            if (fabs(d) <= athr) ph[r][(t + kW) >> 5] |= 1u << ((t + kW) & 31);
+            const uint32_t b = __brev(nw[r]);  // bit t = step t (window position t + kW)
+            ph[r][q0] |= b << sh;
+            if constexpr (sh != 0) ph[r][q0 + 1] |= b >> (32 - sh);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const double cv = colc[t + kW];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const double d = __dsub_rn(rowc[r * HS + t + kW], cv);
+              if (fabs(d) <= athr) ph[r][(t + kW) >> 5] |= 1u << ((t + kW) & 31);
+            }
           }
         }
         uint32_t wr[R];

@@ -11,8 +11,9 @@ struct Variant {
   int nw, r;              // warps per CTA, stacked slots (band = r * 32 * nw rows)
   int w;                  // term window (m-1)*tau
   int reuse;              // 1: compile-time (m, tau) with term reuse; 0: direct
-  int prec;               // 0: float64 evaluation; 1: f32 filter (rqa_unit.cuh)
+  int prec;               // 0: float64 evaluation; 1: f32 filter; 2: prefilter (rqa_unit.cuh)
   size_t smem;            // dynamic shared memory bytes
+  int f32pred;            // prefilter with the packed float32 component predicate
   cudaError_t (*launch)(const UnitArgs&, int nunits, int w, cudaStream_t);
   const void* kernel;     // for occupancy queries
   int64_t band_rows() const { return (int64_t)r * 32 * nw; }
@@ -27,7 +28,8 @@ constexpr int min_blocks() {
 
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
-  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>);
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>,
+                  kF32Pred<PREC, M, R>);
   auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(), PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
@@ -38,8 +40,8 @@ cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>);
-  return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total,
+  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>, kF32Pred<PREC, M, R>);
+  return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total, kF32Pred<PREC, M, R> ? 1 : 0,
                  &launch_unit<METRIC, M, TAU, NW, R, PREC>,
                  (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(),
                                            PREC>};
