@@ -187,8 +187,8 @@ int validate(int64_t len, int32_t m, int32_t tau, int32_t metric, double radius,
            RQA_ESHORT;
   p->len = len;
   p->n = len - span;
-  if (p->n > (int64_t)1 << 31)
-    return set_err(err, errlen, "n_vectors %lld exceeds 2^31", (long long)p->n), RQA_EINVAL;
+  if (p->n >= (int64_t)1 << 28)  // run lengths travel in 28 bits (rqa_runs.cuh events)
+    return set_err(err, errlen, "n_vectors %lld exceeds 2^28 - 1", (long long)p->n), RQA_EINVAL;
   p->m = m;
   p->tau = tau;
   p->metric = metric;
@@ -1042,13 +1042,15 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
   const int hblocks = (int)std::min<size_t>((hcount + 255) / 256, 148 * 8);
   for (int g = 0; g < G; ++g) {
     const StripeJob& j = jobs[g];
-    RQA_CUDA(cudaMemcpyPeerAsync(gpre + g * n, j0.dev, j.pre, j.dev, n * 4, st), "gather");
-    RQA_CUDA(cudaMemcpyPeerAsync(gsuf + g * n, j0.dev, j.suf, j.dev, n * 4, st), "gather");
-    RQA_CUDA(cudaMemcpyPeerAsync(gcol + g * 2 * n, j0.dev, j.col, j.dev, 2 * n * 4, st), "gather");
-    if (j.hi > j.lo)
+    if (j.hi > j.lo) {  // an empty stripe has no summaries (the stitch skips it)
+      RQA_CUDA(cudaMemcpyPeerAsync(gpre + g * n, j0.dev, j.pre, j.dev, n * 4, st), "gather");
+      RQA_CUDA(cudaMemcpyPeerAsync(gsuf + g * n, j0.dev, j.suf, j.dev, n * 4, st), "gather");
+      RQA_CUDA(cudaMemcpyPeerAsync(gcol + g * 2 * n, j0.dev, j.col, j.dev, 2 * n * 4, st),
+               "gather");
       RQA_CUDA(cudaMemcpyPeerAsync(grow_ + 2 * j.lo, j0.dev, j.row + 2 * j.lo, j.dev,
                                    (size_t)(j.hi - j.lo) * 2 * 4, st),
                "gather");
+    }
     if (g == 0) continue;
     const unsigned long long* src = j.hist;
     if (j.dev != j0.dev) {

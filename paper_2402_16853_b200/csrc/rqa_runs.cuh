@@ -116,14 +116,17 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 // histogram updates run at full SIMD width even when only a few lanes of a
 // pass see a boundary.
 // ---------------------------------------------------------------------------
-constexpr int kQueueCap = 128;  // events per warp (uint4 each)
-// Drain when this many events are queued: every check follows at most 64
-// pushes (two words per lane), so the ring never holds more than 127.
-constexpr uint32_t kDrainAt = 64u;
+constexpr int kQueueCap = 256;  // events per warp (8 bytes each)
+// Drain when this many events are queued: every check follows at most 128
+// pushes (four words per lane), so the ring never holds more than 255.
+constexpr uint32_t kDrainAt = 128u;
 
-// Event: x = boundary mask, y = carried run (len << 1 | bit), z = flags:
-// bit 0 skip the carried run (it is the sequence's first run, kept in the
-// state), bits 1..2 diagonal weight (0: vertical/white sink).
+// Event (8 bytes): x = boundary mask, y = carried run (len << 1 | bit) in
+// bits 0..28 plus flags in bits 29..31: bit 29 skip the carried run (it is
+// the sequence's first run, kept in the state), bits 30..31 diagonal weight
+// (0: vertical/white sink).  Runs are shorter than 2^28 (validate() bounds n).
+constexpr uint32_t kEvCurBits = 29;
+constexpr uint32_t kEvCurMask = (1u << kEvCurBits) - 1u;
 // Shared word just past the histogram bins and the kernel's two mbarriers
 // (SymSmem reserves it): the target of the zero-weight / out-of-range adds.
 constexpr uint32_t kDummyBin = 3u * kSmemBins + 4u;
@@ -139,17 +142,19 @@ __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint3
   if (!small && w) atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
 }
 
-__device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
+__device__ __forceinline__ void expand_event(uint2 e, const Hist& h) {
   uint32_t bnd = e.x;
-  const uint32_t w = e.z >> 1;
+  const uint32_t flags = e.y >> kEvCurBits;
+  const uint32_t w = flags >> 1;
+  const uint32_t ecur = e.y & kEvCurMask;
   // weight and histogram row of runs of zeroes / ones
   const uint32_t w0 = (w == 0u) ? 1u : 0u, w1 = (w == 0u) ? 1u : w;
   const uint32_t k0 = kWhite, k1 = (w == 0u) ? (uint32_t)kVert : (uint32_t)kDiag;
-  uint32_t bit = e.y & 1u;
+  uint32_t bit = ecur & 1u;
   // first closed run: carried length + first boundary position
   uint32_t p = (uint32_t)__ffs(bnd) - 1u;
-  uint32_t len = (e.y >> 1) + p;
-  uint32_t wt = (e.z & 1u) ? 0u : (bit ? w1 : w0);
+  uint32_t len = (ecur >> 1) + p;
+  uint32_t wt = (flags & 1u) ? 0u : (bit ? w1 : w0);
   for (;;) {
     hist_red(h, bit ? k1 : k0, len, wt);  // wt == 0: predicated off
     bnd &= bnd - 1u;
@@ -163,7 +168,7 @@ __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
 }
 
 struct EventQueue {
-  uint4* ring;       // this warp's kQueueCap entries
+  uint2* ring;       // this warp's kQueueCap entries
   uint32_t head;     // warp-uniform
   uint32_t tail;     // warp-uniform
   uint32_t lt_mask;  // (1 << lane) - 1
@@ -181,10 +186,10 @@ static __device__ __noinline__ uint32_t queue_drain_impl(uint32_t ring_sa, uint3
   while (tail - head >= 32u || (all && tail != head)) {
     const uint32_t avail = tail - head;
     if ((uint32_t)lane < avail) {
-      uint4 e;
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
-                   : "r"(ring_sa + 16u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
+      uint2 e;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                   : "=r"(e.x), "=r"(e.y)
+                   : "r"(ring_sa + 8u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
       expand_event(e, h);
     }
     head += avail < 32u ? avail : 32u;
@@ -222,9 +227,9 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
   // no generic-address rematerialisation per push
   const uint32_t slot = (q.tail + __popc(m & q.lt_mask)) & (uint32_t)(kQueueCap - 1);
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
-      "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(q.ring_sa + 16u * slot),
-      "r"(bnd), "r"(cur), "r"((diag_weight << 1) | (mkfirst ? 1u : 0u)), "r"(0u),
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(q.ring_sa + 8u * slot),
+      "r"(bnd), "r"(cur | (((diag_weight << 1) | (mkfirst ? 1u : 0u)) << kEvCurBits)),
       "r"(ev ? 1u : 0u));  // no memory clobber: the ring is only accessed through asm
   q.tail += __popc(m);
 }

@@ -103,7 +103,7 @@ struct SymSmem {
     off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
     off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
     off_queue = off_rowst + (size_t)R * D * sizeof(uint2);
-    off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
+    off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint2);
     // bins, two mbarriers (16 B), the dummy bin of hist_red (16 B reserved)
     off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
     off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
@@ -137,8 +137,9 @@ __device__ __forceinline__ void diag_finish(const RunState& st, bool open, uint1
   *Pk = (uint16_t)(run_bit(first) ? run_len(first) : 0u);
   if (open) {
     *Sk = (uint16_t)(run_bit(g.last) ? run_len(g.last) : 0u);
-  } else if (!g.uniform) {
-    sink(g.last);
+  } else {
+    *Sk = 0u;  // never continued (the fold ignores it); written so every entry is defined
+    if (!g.uniform) sink(g.last);
   }
 }
 

@@ -200,7 +200,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   uint32_t rowbuf_sa = smem_u32(rowbuf + wv * H + lane);
   int skip = a.skip;
   asm volatile("" : "+r"(rowbuf_sa), "+r"(skip));
-  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
+  EventQueue evq{reinterpret_cast<uint2*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
   evq.ring_sa = smem_u32(evq.ring);
   uint16_t* Pslot[R];
@@ -350,8 +350,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 
     // the R words of chunk c are final: their transposed row words go to
     // rowbuf (the R transposes are independent and interleave), then the
-    // diagonal runs of their 32 rows; the event ring is drained after every
-    // second slot (<= 63 queued + 2 x 32 pushed < kQueueCap)
+    // diagonal runs of their 32 rows; one drain check after the R <= 4
+    // pushes (<= 127 queued + 4 x 32 pushed < kQueueCap)
     auto finish_chunk = [&](int c, uint32_t (&w)[R]) {
       uint32_t tw[R];
 #pragma unroll
@@ -378,9 +378,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
             st[r] = RunState{1u, 0u};
           }
         }
-        if ((r & 1) || r == R - 1)
-          if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
       }
+      if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
     };
 
     if constexpr (kPre) {
@@ -750,13 +749,17 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           rs[p] = RunState{rsv.x, rsv.y};
         }
         if (__all_sync(0xffffffffu, all_full)) {
-#pragma unroll 2
-          for (int v = 0; v < NW; ++v) {
+          static_assert(NW % 2 == 0 && PR <= 2, "row phase: 2 x PR pushes per drain check");
+#pragma unroll 1
+          for (int v = 0; v < NW; v += 2) {
 #pragma unroll
-            for (int p = 0; p < PR; ++p) {
-              const uint32_t w = rowbuf[v * H + lr[p]];
-              pts += __popc(w);
-              runs_push(w, 32, rs[p], 0u, evq);
+            for (int vv = 0; vv < 2; ++vv) {
+#pragma unroll
+              for (int p = 0; p < PR; ++p) {
+                const uint32_t w = rowbuf[(v + vv) * H + lr[p]];
+                pts += __popc(w);
+                runs_push(w, 32, rs[p], 0u, evq);
+              }
             }
             if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
           }
@@ -826,7 +829,20 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
                 runs_push(bits, nb, cur[p], 0u, evq);
               }
             }
-            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+          };
+          // windows c = hi, hi-1, ..., lo (descending), two per drain check
+          auto col_steps = [&](int hi, int lo, const int* lim, auto full) {
+            int c = hi;
+#pragma unroll 1
+            for (; c - 1 >= lo; c -= 2) {
+              col_step(c, lim, full);
+              col_step(c - 1, lim, full);
+              if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+            }
+            if (c >= lo) {
+              col_step(c, lim, full);
+              if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+            }
           };
           using kFull = std::integral_constant<bool, true>;
           using kPart = std::integral_constant<bool, false>;
@@ -840,13 +856,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           ffin = __all_sync(0xffffffffu, ffin);
           // windows above the warp's own start the columns of iteration x+1
           if (do_new) {
-            if (fnew) {
-#pragma unroll 1
-              for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new, kFull{});
-            } else {
-#pragma unroll 1
-              for (int c = NCH - 1; c > wv; --c) col_step(c, lim_new, kPart{});
-            }
+            if (fnew) col_steps(NCH - 1, wv + 1, lim_new, kFull{});
+            else col_steps(NCH - 1, wv + 1, lim_new, kPart{});
           }
 #pragma unroll
           for (int p = 0; p < PR; ++p) {
@@ -855,13 +866,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
           // the warp's own window and those below finish the columns of x
           if (do_fin) {
-            if (ffin) {
-#pragma unroll 1
-              for (int c = wv; c >= 0; --c) col_step(c, lim_fin, kFull{});
-            } else {
-#pragma unroll 1
-              for (int c = wv; c >= 0; --c) col_step(c, lim_fin, kPart{});
-            }
+            if (ffin) col_steps(wv, 0, lim_fin, kFull{});
+            else col_steps(wv, 0, lim_fin, kPart{});
           }
 #pragma unroll
           for (int p = 0; p < PR; ++p) fin[p] = cur[p];
