@@ -64,10 +64,9 @@ __host__ __device__ __forceinline__ uint32_t pack_col(uint32_t top, uint32_t bot
   return ((top & 0xffffu) << 16) | (bot & 0xffffu);
 }
 
-// Capacity (power of two) of a warp's streaming candidate list (prefilter
-// kernels): pending candidates plus one chunk's; a denser chunk is resolved
-// per lane.  256 keeps two CTAs per SM.
-constexpr int kCandCap = 256;
+// Capacities (powers of two) of a warp's streaming candidate list (prefilter
+// kernels) are per variant (rqa_unit.cuh kCandCapOf): pending entries plus
+// one slot word's; a denser word is resolved per lane.
 
 struct SymSmem {
   int H, HS, D, W, CW;
@@ -77,11 +76,11 @@ struct SymSmem {
   // esize 8: float64 row/column windows; 4: float32 windows (f32 filter
   // kernels), the row window stored as R/2 interleaved slot pairs of
   // HS + W + 4 float2 each (rqa_unit.cuh, packed f32x2 evaluation).
-  // coop: per-warp streaming candidate list (prefilter kernels)
+  // cand_cap: entries of the per-warp streaming candidate list (prefilter kernels)
   // f32pred: float32 copies of the windows for the packed prefilter
   // predicate (row window as R/2 slot pairs of HS + W + 4 float2, two float
   // column buffers), appended at the end
-  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, bool coop = false,
+  __host__ __device__ SymSmem(int NW, int R, int W_, int esize = 8, int cand_cap = 0,
                               bool f32pred = false) {
     D = 32 * NW;
     HS = D;
@@ -106,7 +105,7 @@ struct SymSmem {
     off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint2);
     // bins, two mbarriers (16 B), the dummy bin of hist_red (16 B reserved)
     off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
-    off_cres = off_cand + (coop ? (size_t)NW * kCandCap * sizeof(uint16_t) : 0);
+    off_cres = off_cand + (size_t)NW * cand_cap * sizeof(uint16_t);
     total = off_cres;
     CWF = ((HS + D + W + 4) + 3) & ~3;
     off_rowf = off_colf0 = off_colf1 = total;

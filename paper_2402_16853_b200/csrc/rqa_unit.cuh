@@ -107,9 +107,12 @@ __device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int
 
 // Prefilter kernels (PREC 2) resolve their candidates warp-cooperatively from
 // a per-warp list that streams across the chunks of an iteration: every
-// round takes 32 candidates at full SIMD width (rqa_unit.cuh, phase 1).
+// round takes 32 entries at full SIMD width (rqa_unit.cuh, phase 1).  Short
+// sums list candidate words (at most R * 32 new entries per chunk, 256
+// entries); long sums (m >= 5) list cells, appended per slot word, 512
+// entries (two CTAs per SM still fit).
 template <int PREC, int M>
-constexpr bool kCoopResolve = (PREC == 2);
+constexpr int kCandCapOf = (PREC != 2) ? 0 : (M <= 4 ? 256 : 512);
 // Short-window prefilter kernels evaluate the per-component predicate in
 // packed float32 (sub/fma.rn.f32x2 over slot pairs, the sign bit of
 // d32*d32 - D32^2 funnel-shifted into the word): 2.5 instructions per cell
@@ -150,7 +153,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   constexpr int RP = (R + 1) / 2;  // slot pairs
   const int W = kDirect ? W_rt : kW;
   constexpr bool kFP = kF32Pred<PREC, M, R>;
-  const SymSmem L(NW, R, W, (int)sizeof(F), kCoopResolve<PREC, M>, kFP);
+  constexpr int kCandCap = kCandCapOf<PREC, M>;
+  const SymSmem L(NW, R, W, (int)sizeof(F), kCandCap, kFP);
   const int PS = HS + W + 4;       // packed row window: float2 elements per slot pair
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -475,7 +479,6 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
         }
         uint32_t wr[R];
-        int kc = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           uint32_t w = ph[r][0];
@@ -488,7 +491,6 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           ph[r][NPH - 1] = 0u;
           w = kdr[r] < theiler ? 0u : w;  // Theiler-excluded cells need no sum
           wr[r] = w;
-          kc += __popc(w);
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
                        "r"(w)
                        : "memory");
@@ -510,17 +512,19 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
           continue;
         }
-        int incl = kc;
+        // cell list: one slot word at a time (fewer list overflows than per chunk)
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t tot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
-        if (ltail - lhead + tot <= (uint32_t)kCandCap) {
-          uint32_t pos = ltail + (uint32_t)(incl - kc);
+        for (int r = 0; r < R; ++r) {
+          const int kr = __popc(wr[r]);
+          int incl = kr;
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const uint32_t tot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+          if (ltail - lhead + tot <= (uint32_t)kCandCap) {
+            uint32_t pos = ltail + (uint32_t)(incl - kr);
             uint32_t w = wr[r];
             while (w) {
               const int t = __ffs(w) - 1;
@@ -528,17 +532,14 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               cl[pos++ & (uint32_t)(kCandCap - 1)] =
                   (uint16_t)((r << 13) | (c << 10) | (lane << 5) | t);
             }
-          }
-          ltail += tot;
-          __syncwarp();
-          while (ltail - lhead >= 32u) {
-            resolve_round(lhead, 32u);
-            lhead += 32u;
-          }
-        } else {
-          // dense chunk: every lane resolves its own candidates
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
+            ltail += tot;
+            __syncwarp();
+            while (ltail - lhead >= 32u) {
+              resolve_round(lhead, 32u);
+              lhead += 32u;
+            }
+          } else {
+            // dense slot word: every lane resolves its own candidates
             uint32_t cand = wr[r], res = wr[r];
             while (cand) {
               const int t = __ffs(cand) - 1;

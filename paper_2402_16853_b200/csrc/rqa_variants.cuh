@@ -28,7 +28,7 @@ constexpr int min_blocks() {
 
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
-  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>,
+  const SymSmem L(NW, R, M == 0 ? w : (M - 1) * TAU, PREC == 1 ? 4 : 8, kCandCapOf<PREC, M>,
                   kF32Pred<PREC, M, R>);
   auto k = unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(), PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
@@ -40,7 +40,7 @@ cudaError_t launch_unit(const UnitArgs& a, int nunits, int w, cudaStream_t st) {
 template <int METRIC, int M, int TAU, int NW, int R, int PREC = 0>
 Variant make_variant(int w_rt) {
   const int w = (M == 0) ? w_rt : (M - 1) * TAU;
-  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8, kCoopResolve<PREC, M>, kF32Pred<PREC, M, R>);
+  const SymSmem L(NW, R, w, PREC == 1 ? 4 : 8, kCandCapOf<PREC, M>, kF32Pred<PREC, M, R>);
   return Variant{NW, R, w, M == 0 ? 0 : 1, PREC, L.total, kF32Pred<PREC, M, R> ? 1 : 0,
                  &launch_unit<METRIC, M, TAU, NW, R, PREC>,
                  (const void*)&unit_kernel<METRIC, M, TAU, NW, R, min_blocks<M, TAU, NW, R>(),
