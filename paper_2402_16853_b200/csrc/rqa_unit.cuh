@@ -388,25 +388,14 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
 
     if constexpr (kPre) {
       // ---- phase 1: candidate words (AND of the m shifted predicates
-      // |d| <= D*) of every chunk go to this lane's rowbuf slots; their set
-      // bits are appended to the warp's candidate list, which is resolved 32
-      // at a time (exact float64 sums in the reference's order) as soon as
-      // a full round is queued.  A failing candidate clears its bit.
+      // |d| <= D*) of every chunk go to this lane's rowbuf slots.  Their
+      // candidates are resolved 32 at a time (exact float64 sums in the
+      // reference's order) from a streaming list: per warp, nonzero words,
+      // as the chunks are evaluated (m <= 4); CTA-wide, cells, after all
+      // warps evaluated (m >= 5, phase 1b).  A failing candidate clears its bit.
       static_assert(R <= 4 && NCH <= 8, "candidate encoding: 2-bit slot, 3-bit chunk");
       uint16_t* cl = reinterpret_cast<uint16_t*>(smem + L.off_cand) + wv * kCandCap;
       const uint32_t wbase = smem_u32(rowbuf + wv * H);  // this warp's rowbuf words
-      auto resolve_round = [&](uint32_t head, uint32_t avail) {
-        if ((uint32_t)lane < avail) {
-          const uint32_t e = cl[(head + (uint32_t)lane) & (uint32_t)(kCandCap - 1)];
-          const int r = (int)(e >> 13), ce = (int)((e >> 10) & 7u), sl = (int)((e >> 5) & 31u),
-                    t = (int)(e & 31u);
-          const int off = r * HS + 32 * ce;
-          if (!pre_exact(s_row + off + t, s_col - lane + sl + 32 * ce + t)) {
-            const uint32_t addr = wbase + 4u * (uint32_t)(off + sl);
-            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(~(1u << t)) : "memory");
-          }
-        }
-      };
       uint32_t lhead = 0u, ltail = 0u;  // warp-uniform list cursors
       // short sums (m <= 4): the list holds nonzero candidate WORDS (slot,
       // chunk, lane); the lane that takes an entry resolves every candidate
@@ -512,10 +501,43 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           }
           continue;
         }
-        // cell list: one slot word at a time (fewer list overflows than per chunk)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int kr = __popc(wr[r]);
+      }
+      if constexpr (kWordList) {
+        __syncwarp();
+        while (ltail != lhead) {  // the last, partial round
+          const uint32_t avail = min(ltail - lhead, 32u);
+          resolve_words(lhead, avail);
+          lhead += avail;
+        }
+        __syncwarp();
+      } else {
+        // ---- phase 1b (long sums): the candidate cells of the whole CTA are
+        // resolved by all warps.  Word group g = (source warp ws, slot r,
+        // chunk c) goes to warp (ws + r * NCH + c) % NW, so every warp gets an
+        // equal share of every source warp's groups (the candidate density
+        // varies across diagonals, i.e. across warps).  Entries: group index
+        // gi = r * NCH + c (5 bits), lane, step.
+        static_assert(R * NCH <= 32 && (NW & (NW - 1)) == 0, "group encoding");
+        __syncthreads();  // every warp's candidate words are in rowbuf
+        const F* colbase = s_col - delta;  // column window of lane 0 of warp 0
+        auto resolve_cells = [&](uint32_t head, uint32_t avail) {
+          if ((uint32_t)lane < avail) {
+            const uint32_t e = cl[(head + (uint32_t)lane) & (uint32_t)(kCandCap - 1)];
+            const int gi = (int)(e >> 10), sl = (int)((e >> 5) & 31u), t = (int)(e & 31u);
+            const int r = gi / NCH, ce = gi % NCH, ws = (wv - gi) & (NW - 1);
+            const int off = r * HS + 32 * ce;
+            if (!pre_exact(s_row + off + t, colbase + 32 * ws + sl + 32 * ce + t)) {
+              const uint32_t addr = smem_u32(rowbuf + ws * H + off + sl);
+              asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(~(1u << t)) : "memory");
+            }
+          }
+        };
+#pragma unroll 1
+        for (int gi = 0; gi < R * NCH; ++gi) {
+          const int r = gi / NCH, ce = gi % NCH, ws = (wv - gi) & (NW - 1);
+          const int off = r * HS + 32 * ce;
+          const uint32_t w = rowbuf[ws * H + off + lane];
+          const int kr = __popc(w);
           int incl = kr;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -525,41 +547,38 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           const uint32_t tot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
           if (ltail - lhead + tot <= (uint32_t)kCandCap) {
             uint32_t pos = ltail + (uint32_t)(incl - kr);
-            uint32_t w = wr[r];
-            while (w) {
-              const int t = __ffs(w) - 1;
-              w &= w - 1u;
-              cl[pos++ & (uint32_t)(kCandCap - 1)] =
-                  (uint16_t)((r << 13) | (c << 10) | (lane << 5) | t);
+            uint32_t ww = w;
+            while (ww) {
+              const int t = __ffs(ww) - 1;
+              ww &= ww - 1u;
+              cl[pos++ & (uint32_t)(kCandCap - 1)] = (uint16_t)((gi << 10) | (lane << 5) | t);
             }
             ltail += tot;
             __syncwarp();
             while (ltail - lhead >= 32u) {
-              resolve_round(lhead, 32u);
+              resolve_cells(lhead, 32u);
               lhead += 32u;
             }
           } else {
-            // dense slot word: every lane resolves its own candidates
-            uint32_t cand = wr[r], res = wr[r];
+            // dense word set: every lane resolves its own word of the group
+            uint32_t cand = w, res = w;
             while (cand) {
               const int t = __ffs(cand) - 1;
               cand &= cand - 1u;
-              if (!pre_exact(rowc + r * HS + t, colc + t)) res &= ~(1u << t);
+              if (!pre_exact(s_row + off + t, colbase + 32 * ws + lane + 32 * ce + t))
+                res &= ~(1u << t);
             }
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c)),
-                         "r"(res)
-                         : "memory");
+            rowbuf[ws * H + off + lane] = res;
           }
         }
+        __syncwarp();
+        while (ltail != lhead) {  // the last, partial round
+          const uint32_t avail = min(ltail - lhead, 32u);
+          resolve_cells(lhead, avail);
+          lhead += avail;
+        }
+        __syncthreads();  // resolved words visible to their owners
       }
-      __syncwarp();
-      while (ltail != lhead) {  // the last, partial round
-        const uint32_t avail = min(ltail - lhead, 32u);
-        if constexpr (kWordList) resolve_words(lhead, avail);
-        else resolve_round(lhead, avail);
-        lhead += avail;
-      }
-      __syncwarp();
       // ---- phase 2: final words -> diagonal runs, transposed row words
       for (int c = 0; c < NCH; ++c) {
         uint32_t w[R];
