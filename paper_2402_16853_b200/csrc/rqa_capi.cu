@@ -105,6 +105,8 @@ struct Workspace {
   size_t rowlead_cap = 0;
   uint2* rowpiece = nullptr;   // [nunits][H]
   size_t rowpiece_cap = 0;
+  uint2* drec = nullptr;       // [nunits][R-1][D] diagonal pieces cut at unit ends
+  size_t drec_cap = 0;
   Unit* units = nullptr;       // [nunits] launch order
   size_t units_cap = 0;
   int4* units_bb = nullptr;    // [nunits] sorted by band, xa
@@ -514,7 +516,9 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   pl.band_start.assign(nb + 1, 0);
   for (int64_t b = 0; b < nb; ++b) {
     pl.band_start[b] = (int32_t)pl.by_band.size();
-    const int64_t parts = std::max<int64_t>(1, (X[b] + len - 1) / len);
+    // every unit spans >= R iterations: a diagonal's band segment (R
+    // consecutive iterations) is then cut by at most one unit boundary
+    const int64_t parts = std::max<int64_t>(1, std::min((X[b] + len - 1) / len, X[b] / R));
     for (int64_t q = 0; q < parts; ++q) {
       const int32_t xa = (int32_t)(X[b] * q / parts), xb = (int32_t)(X[b] * (q + 1) / parts);
       const int32_t idx = (int32_t)pl.units.size();
@@ -528,11 +532,12 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   return pl;
 }
 
+// Band-level summaries: P and S (uint16) and the column part (uint32) per
+// (band, diagonal / column): 8 bytes per entry of the compact layout.
 int64_t unit_workspace_bytes(const Problem& p, int64_t row_lo, int64_t row_hi) {
-  const int64_t H = p.var.band_rows(), HS = p.var.slot_rows();
+  const int64_t H = p.var.band_rows();
   const int64_t nb = (row_hi - row_lo + H - 1) / H;
-  const int64_t nslots = (row_hi - row_lo + HS - 1) / HS;
-  return 2 * slot_offset(nslots, p.n, row_lo, HS) * 2 + sym_band_offset(nb, p.n, row_lo, H) * 4;
+  return sym_band_offset(nb, p.n, row_lo, H) * 8;
 }
 
 // Work-unit kernel over rows [row_lo, row_hi) + folds.
@@ -556,10 +561,11 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
            "occupancy");
   const UnitPlan pl = plan_units(p, row_lo, row_hi, sms * std::max(1, per_sm));
   const int64_t nunits = (int64_t)pl.units.size();
-  const int64_t nslots = (row_hi - row_lo + HS - 1) / HS;
-  const int64_t ptot = slot_offset(nslots, p.n, row_lo, HS);
   const int64_t ctot = sym_band_offset(nb, p.n, row_lo, H);
-  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * ptot)), "allocating diagonal summaries");
+  const int64_t D = p.var.slot_rows(), R = p.var.r;
+  RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * ctot)), "allocating diagonal summaries");
+  RQA_CUDA(grow(&ws->drec, &ws->drec_cap, (size_t)(nunits * std::max<int64_t>(R - 1, 1) * D)),
+           "allocating diagonal records");
   RQA_CUDA(grow(&ws->cs, &ws->cs_cap, (size_t)ctot), "allocating column summaries");
   RQA_CUDA(grow(&ws->rowpiece, &ws->rowpiece_cap, (size_t)(nunits * H)), "allocating row pieces");
   RQA_CUDA(grow(&ws->units, &ws->units_cap, (size_t)nunits), "allocating units");
@@ -592,8 +598,8 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.theiler = p.theiler;
   a.m = p.m;
   a.tau = p.tau;
-  a.P = ws->ps;               // [2][ptot]: P then S, per-slot compact layout
-  a.S = ws->ps + ptot;
+  a.P = ws->ps;               // [2][ctot]: P then S, band-level compact layout
+  a.S = ws->ps + ctot;
   a.colsum = ws->cs;
   a.rowlead = nullptr;
   a.hist = hist;
@@ -612,11 +618,33 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.pre_negd2 = p.pre_negd2;
   ua.units = ws->units;
   ua.rowpiece = ws->rowpiece;
+  ua.drec = ws->drec;
   RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
   g_launches++;
   if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
 
   const int threads = 256;
+  if (R > 1 && nunits > nb) {  // some band is cut into several units
+    DiagPieceArgs dp;
+    dp.units_by_band = ws->units_bb;
+    dp.nunits = (int)nunits;
+    dp.drec = ws->drec;
+    dp.P = a.P;
+    dp.S = a.S;
+    dp.row_lo = row_lo;
+    dp.row_hi = row_hi;
+    dp.n = p.n;
+    dp.H = H;
+    dp.HS = HS;
+    dp.D = D;
+    dp.R = (int)R;
+    dp.hist = hist;
+    const int64_t recs = nunits * (R - 1) * D;
+    fix_diag_pieces<<<(int)std::min<int64_t>((recs + threads - 1) / threads, 148 * 16), threads, 0,
+                      st>>>(dp);
+    RQA_CUDA(cudaGetLastError(), "launching diagonal piece join");
+    g_launches++;
+  }
   const int64_t blocks = std::min<int64_t>((p.n + threads - 1) / threads, 148 * 16);
   SymFoldArgs f;
   memset(&f, 0, sizeof f);
@@ -624,8 +652,8 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   f.S = a.S;
   f.row_lo = row_lo;
   f.row_hi = row_hi;
-  f.H = HS;                   // diagonal segments are slots
-  f.nb = (int)nslots;
+  f.H = H;                    // diagonal segments are bands
+  f.nb = (int)nb;
   f.n = p.n;
   f.hist = hist;
   f.out_p = out_p;
@@ -1227,6 +1255,7 @@ int rqa_release(void) {
     cudaFree(ws->cs);
     cudaFree(ws->rowlead);
     cudaFree(ws->rowpiece);
+    cudaFree(ws->drec);
     cudaFree(ws->units);
     cudaFree(ws->units_bb);
     cudaFree(ws->band_start);

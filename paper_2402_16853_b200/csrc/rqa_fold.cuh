@@ -222,6 +222,61 @@ __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, 
   fb.flush(a.hist, n);
 }
 
+// Diagonal band segments cut by a work-unit boundary (rqa_unit.cuh): unit u
+// walked the upper part (slots 0..rA, open at the cut) and unit u+1 of the
+// same band the lower part; join the two halves into the band-level P/S the
+// diagonal fold reads, counting the run that meets at the cut (or, for a
+// segment cut by the matrix's right edge, the last run).  One thread per
+// (unit, rA, lane) record; the geometry decides which records were written.
+struct DiagPieceArgs {
+  const int4* units_by_band;  // (band, xa, xb, idx) in idx order
+  int nunits;
+  const uint2* drec;          // [nunits][R-1][D]
+  uint16_t* P;                // band-level compact layout (height H)
+  uint16_t* S;
+  int64_t row_lo, row_hi, n, H, HS, D;
+  int R;
+  unsigned long long* hist;
+};
+
+__global__ void fix_diag_pieces(const DiagPieceArgs a) {
+  const int64_t per = (int64_t)(a.R - 1) * a.D;
+  const int64_t total = (int64_t)a.nunits * per;
+  const GHist h{a.hist, a.n + 1};
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(q / per);
+    const int rA = (int)((q % per) / a.D);
+    const int delta = (int)(q % a.D);
+    const int4 U = a.units_by_band[u];
+    if (u + 1 >= a.nunits || a.units_by_band[u + 1].x != U.x) continue;  // last unit of its band
+    const int64_t i0 = a.row_lo + (int64_t)U.x * a.H;
+    const int64_t hrows = min(i0 + a.H, a.row_hi) - i0;
+    const int64_t nrem = a.n - i0;
+    const int64_t kd = (int64_t)(U.z - 1) * a.D - (int64_t)rA * a.HS + delta;
+    if (kd < 0 || kd >= nrem) continue;
+    const int64_t brows = min(hrows, nrem - kd);
+    if (rA >= (brows - 1) / a.HS) continue;  // the segment ended inside unit u
+    const uint2 rec = a.drec[q];
+    const int64_t LA = (int64_t)(rA + 1) * a.HS, LB = brows - LA;
+    const int64_t PA = rec.x & 0xffffu, SA = rec.x >> 16;
+    const int64_t PB = rec.y & 0xffffu, SB = (rec.y >> 16) & 0x7fffu;
+    const bool open = (rec.y >> 31) == 0u;
+    const bool allA = PA == LA, allB = PB == LB;
+    const uint32_t w = kd == 0 ? 1u : 2u;
+    const int64_t Pv = allA ? LA + PB : PA;
+    const int64_t Sv = !open ? 0 : allB ? SA + LB : SB;
+    if (!allA && !allB) {
+      if (SA + PB > 0) h.add(kDiag, SA + PB, w);  // the run meeting at the cut
+    } else if (!open && allB && !allA) {
+      h.add(kDiag, SA + LB, w);  // last run, ends at the matrix edge
+    }
+    const int64_t off = sym_band_offset(U.x, a.n, a.row_lo, a.H) + kd;
+    a.P[off] = (uint16_t)Pv;
+    a.S[off] = (uint16_t)Sv;
+  }
+}
+
 // Final fold over stripes (multi-GPU) for the work-unit layout.
 struct UnitStitchArgs {
   const int32_t* sp;        // [nseg][n] diagonal prefix

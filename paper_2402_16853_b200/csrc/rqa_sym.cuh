@@ -125,21 +125,21 @@ __device__ __forceinline__ void setbit_le(uint32_t& dw, double acc, double thr, 
       : "d"(acc), "d"(thr), "r"(bit));
 }
 
-// A diagonal's segment inside the band ends: report its band-top run as P
-// (length if it is a run of ones, else 0) and, if the segment ends at the
-// band's bottom edge (open), its bottom run as S; a segment cut by the
-// matrix's right edge (closed) counts its last run here.
-__device__ __forceinline__ void diag_finish(const RunState& st, bool open, uint16_t* Pk,
-                                            uint16_t* Sk, const LineSink& sink) {
+// A piece of a diagonal ends: returns P | S << 16, P = its top run (length if
+// it is a run of ones, else 0) and, if the piece ends at the band's bottom
+// edge or at a work-unit boundary (open), S = its bottom run; a piece cut by
+// the matrix's right edge (closed) counts its last run here and reports S = 0.
+__device__ __forceinline__ uint32_t diag_piece_end(const RunState& st, bool open,
+                                                   const LineSink& sink) {
   const Seg g = runs_finish(st);
-  const uint32_t first = g.first;
-  *Pk = (uint16_t)(run_bit(first) ? run_len(first) : 0u);
+  const uint32_t p = run_bit(g.first) ? run_len(g.first) : 0u;
+  uint32_t s = 0u;
   if (open) {
-    *Sk = (uint16_t)(run_bit(g.last) ? run_len(g.last) : 0u);
-  } else {
-    *Sk = 0u;  // never continued (the fold ignores it); written so every entry is defined
-    if (!g.uniform) sink(g.last);
+    s = run_bit(g.last) ? run_len(g.last) : 0u;
+  } else if (!g.uniform) {
+    sink(g.last);
   }
+  return p | (s << 16);
 }
 
 }  // namespace rqa

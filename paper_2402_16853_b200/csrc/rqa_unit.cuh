@@ -5,9 +5,12 @@
 // so that every CTA gets a bounded amount of work, which balances the SMs
 // for any n and lets a GPU's share of a multi-GPU run be spread over all of
 // its SMs.  What crosses a unit boundary is stitched by the folds:
-//   * diagonals: every (band, slot) is its own segment of HS rows; the run
-//     state starts at the slot's top row in every iteration and leaves through
-//     its bottom (P/S per slot, compact layout with height HS);
+//   * diagonals: diagonal kd meets slot r of a band at iteration kd/D + r, in
+//     the same lane, so its run state is handed from slot r to slot r+1 in
+//     registers and the whole band segment is one piece (P/S per band,
+//     compact layout with height H).  A work-unit boundary cuts the pieces
+//     of at most R-1 slots per lane; both halves go to a record and
+//     fix_diag_pieces (rqa_fold.cuh) joins them (units span >= R iterations);
 //   * row parts of hooks: each unit reports the first and last run of the
 //     piece of the row it covers (rowpiece[unit][row]);
 //   * column parts of hooks: a column's slot segment spans iterations x-1 and
@@ -32,14 +35,9 @@ struct UnitArgs {
   SymArgs base;            // s, n, row range, thr, theiler, m, tau, P, S, colsum, hist, points
   const Unit* units;       // [nunits], ordered largest work first
   uint2* rowpiece;         // [nunits][H]: (first, last) run of each row's piece
+  uint2* drec;             // [nunits][R-1][D]: diagonal pieces cut at the unit's end
+                           // (x: upper half P | S << 16, y: lower half P | S << 16 | closed << 31)
 };
-
-// Compact offset of per-slot diagonal segments: slot g covers rows
-// [row_lo + g*HS, +HS) and diagonals kd in [0, n - row_g).
-__host__ __device__ __forceinline__ int64_t slot_offset(int64_t g, int64_t n, int64_t row_lo,
-                                                        int64_t HS) {
-  return g * (n - row_lo) - HS * (g * (g - 1) / 2);
-}
 
 // ---------------------------------------------------------------------------
 // f32 filter (PREC = 1).  Cells are evaluated in float32 (packed f32x2 over
@@ -194,7 +192,6 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   };
   const int xa = unit.xa, xb = unit.xb;
   const int xfirst = xa > 0 ? xa - 1 : 0;  // xa-1: recomputed for the columns finishing at xa
-  const int64_t goff0 = b * R;              // global slot index of slot 0
   uint32_t* Cb = a.colsum + band_offset(b, n, a.row_lo, H);
   uint2* piece = ua.rowpiece + (int64_t)unit.idx * H;
   const Hist hist{smem_u32(sh_hist), a.hist, n + 1};
@@ -207,14 +204,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   EventQueue evq{reinterpret_cast<uint2*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
   evq.ring_sa = smem_u32(evq.ring);
-  uint16_t* Pslot[R];
-  uint16_t* Sslot[R];
-  const int64_t ptot = slot_offset((int64_t)((a.row_hi - a.row_lo + HS - 1) / HS), n, a.row_lo, HS);
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    Pslot[r] = a.P + slot_offset(goff0 + r, n, a.row_lo, HS);
-    Sslot[r] = a.P + ptot + slot_offset(goff0 + r, n, a.row_lo, HS);
-  }
+  uint16_t* Pb = a.P + band_offset(b, n, a.row_lo, H);  // band-level diagonal summaries
+  uint16_t* Sb = a.S + band_offset(b, n, a.row_lo, H);
 
   const F* gs;  // samples the windows are staged from
   if constexpr (kF32) gs = a.sf; else gs = a.s;
@@ -313,7 +304,6 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      st[r] = RunState{0u, 0u};  // every (band, slot) is a segment of its own
       if (r == 0 || x == xfirst) {
         if constexpr (!kDirect && kW > 0 && !kPacked) {
           if constexpr (kAnd) {
@@ -334,15 +324,13 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       }
     }
 
-    int kdr[R], lastc[R], openb[R];
+    int kdr[R], lastc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int kd = kx - r * HS + delta;
       kdr[r] = kd;
       const int vrows = min(max(hrows - r * HS, 0), HS);
-      const int crows = min(max(nrem - kd - r * HS, 0), vrows);
-      lastc[r] = crows;
-      openb[r] = (crows == vrows) ? 1 : 0;
+      lastc[r] = min(max(nrem - kd - r * HS, 0), vrows);  // rows of kd in slot r
     }
     // slots whose 32 diagonals all run through all HS rows: every word of the
     // iteration is a full 32-bit pass (warp-uniform fast path of the diagonal runs)
@@ -372,15 +360,11 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         if ((fullmask >> r) & 1u) {
           runs_push(w[r], 32, st[r], kd == 0 ? 1u : 2u, evq);
         } else {
+          // past the diagonal's last row (matrix edge) nothing is consumed;
+          // the piece is closed at the end of the iteration
           const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
           runs_push(w[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq);
-          if (live && !openb[r] && rel >= 0 && rel < 32 && st[r].cur != 0u) {
-            // the segment is cut by the matrix's right edge inside the slot
-            diag_finish(st[r], false, Pslot[r] + kd, Sslot[r] + kd,
-                        LineSink{&hist, kd == 0 ? 1u : 2u});
-            st[r] = RunState{1u, 0u};
-          }
         }
       }
       if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
@@ -485,7 +469,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
                        : "memory");
         }
         if constexpr (kWordList) {
-          // at most R * 32 new entries per chunk: the list never overflows
+          // at most R * 32 new entries per chunk: the list never overflows;
+          // the previous round's reads of reused ring entries come first
+          __syncwarp();
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const uint32_t mk = __ballot_sync(0xffffffffu, wr[r] != 0u);
@@ -536,6 +522,9 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         for (int gi = 0; gi < R * NCH; ++gi) {
           const int r = gi / NCH, ce = gi % NCH, ws = (wv - gi) & (NW - 1);
           const int off = r * HS + 32 * ce;
+          // the last round's list reads precede this group's appends, which
+          // may reuse those ring entries (compute-sanitizer racecheck)
+          __syncwarp();
           const uint32_t w = rowbuf[ws * H + off + lane];
           const int kr = __popc(w);
           int incl = kr;
@@ -905,18 +894,38 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     }
     __syncthreads();
 
-    // ---- every slot's diagonal segment leaves through the slot's bottom edge
+    // ---- diagonal pieces: a band segment ends in the slot holding its last
+    // row (open: the band's last row, it may continue in the next band;
+    // closed: cut by the matrix's right edge); a segment that continues past
+    // the unit's last iteration is handed to the next unit through drec
     if (!warm) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int kd = kdr[r];
-        const int vrows = min(max(hrows - r * HS, 0), HS);
-        // open: the slot's last row is a cell of the diagonal (it may continue)
-        if (kd >= 0 && kd < nrem && vrows > 0 && st[r].cur != 0u &&
-            r * HS + vrows - 1 + kd < nrem)
-          diag_finish(st[r], true, Pslot[r] + kd, Sslot[r] + kd, LineSink{&hist, kd == 0 ? 1u : 2u});
+        if (kd >= 0 && kd < nrem) {
+          const int brows = min(hrows, nrem - kd);  // rows of kd in this band
+          const int rend = (brows - 1) / HS;       // slot of its last row
+          if (r == rend) {
+            const uint32_t ps = diag_piece_end(st[r], brows == hrows,
+                                               LineSink{&hist, kd == 0 ? 1u : 2u});
+            if (x - r >= xa) {  // the whole band segment was walked by this unit
+              Pb[kd] = (uint16_t)(ps & 0xffffu);
+              Sb[kd] = (uint16_t)(ps >> 16);
+            } else {  // lower part of a segment cut at xa (upper part: unit idx-1)
+              ua.drec[((int64_t)(unit.idx - 1) * (R - 1) + (xa - 1 - (x - r))) * D + delta].y =
+                  ps | (brows == hrows ? 0u : 0x80000000u);
+            }
+          } else if (r < rend && x == xb - 1) {  // upper part of a segment cut at xb
+            ua.drec[((int64_t)unit.idx * (R - 1) + r) * D + delta].x =
+                diag_piece_end(st[r], true, LineSink{&hist, 0u});
+          }
+        }
       }
     }
+    // slot r+1 walks slot r's diagonals in the next iteration
+#pragma unroll
+    for (int r = R - 1; r >= 1; --r) st[r] = st[r - 1];
+    st[0] = RunState{0u, 0u};
     if constexpr (kPacked) {  // slot r+1 continues slot r's window (pairs: lo = even slot)
 #pragma unroll
       for (int j = 0; j < kW; ++j) {
