@@ -645,7 +645,8 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
     RQA_CUDA(cudaGetLastError(), "launching diagonal piece join");
     g_launches++;
   }
-  const int64_t blocks = std::min<int64_t>((p.n + threads - 1) / threads, 148 * 16);
+  // fold threads take diagonals / hooks t and n-1-t
+  const int64_t blocks = std::min<int64_t>(((p.n + 1) / 2 + threads - 1) / threads, 148 * 16);
   SymFoldArgs f;
   memset(&f, 0, sizeof f);
   f.P = a.P;

@@ -73,15 +73,20 @@ __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, con
   FoldBins fb{bins};
   fb.init();
   const Hist h{smem_u32(bins), a.hist, n + 1};
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  // a thread folds diagonals t and n-1-t: their segment counts add up to
+  // about the same for every thread (the upper triangle is balanced)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
+       t += (int64_t)gridDim.x * blockDim.x)
+  for (int side = 0; side < 2; ++side) {
+    const int64_t k = side ? n - 1 - t : t;
+    if (side && k == t) break;
     const unsigned long long wgt = (k == 0) ? 1ull : 2ull;
     const int64_t rows = n - k;
     int64_t open = 0, pstr = -1;
     int64_t lo = a.row_lo, off = k, stride = n - a.row_lo;
     const int64_t nseg_k = min((int64_t)a.nb, (rows - a.row_lo + a.H - 1) / a.H);
     // segments in batches: all loads of a batch are issued before the
-    // (sequential) monoid walk, so a thread keeps 2*kFoldBatch loads in flight
+    // (sequential) monoid walk (prefetching the next batch measured slower here)
     for (int64_t g0 = 0; g0 < nseg_k; g0 += kFoldBatch) {
       uint16_t pv[kFoldBatch], sv[kFoldBatch];
 #pragma unroll
@@ -136,8 +141,8 @@ __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, con
 
 // ===========================================================================
 // Folds of the work-unit kernel (rqa_unit.cuh).  Diagonals use sym_fold_diag
-// with per-slot segments (H := HS); hooks combine the per-band column parts
-// with the per-unit row pieces of the row's own band.
+// with per-band segments (after fix_diag_pieces); hooks combine the per-band
+// column parts with the per-unit row pieces of the row's own band.
 // ===========================================================================
 namespace rqa {
 
@@ -160,22 +165,36 @@ __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, 
   FoldBins fb{bins};
   fb.init();
   const Hist h{smem_u32(bins), a.hist, n + 1};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
+  // a thread folds hooks t and n-1-t (balanced band counts, as sym_fold_diag)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
+       t += (int64_t)gridDim.x * blockDim.x)
+  for (int side = 0; side < 2; ++side) {
+    const int64_t c = side ? n - 1 - t : t;
+    if (side && c == t) break;
     // column part: bands above row c
     Seg acc{0u, 0u, 0u};
     {
       int64_t lo = a.row_lo, off = c - a.row_lo, stride = n - a.row_lo;
-      // bands above row c, loads batched as in sym_fold_diag
       const int64_t nbc = c > a.row_lo ? min((int64_t)a.nb, (c - a.row_lo + a.H - 1) / a.H) : 0;
-      for (int64_t g0 = 0; g0 < nbc; g0 += kFoldBatch) {
-        uint32_t vv[kFoldBatch];
+      // batch g is consumed while batch g+1 is loading (the fold is bound by
+      // load latency: one dependent monoid step per band)
+      uint32_t vn[kFoldBatch];
+      auto load = [&](int64_t g0) {
 #pragma unroll
         for (int q = 0; q < kFoldBatch; ++q) {
           // next band: offset grows by (n - lo_g), index shrinks by H
           const int64_t oq = off + q * (stride - a.H) - a.H * (int64_t)(q * (q - 1) / 2);
-          vv[q] = g0 + q < nbc ? a.colsum[oq] : 0u;
+          vn[q] = g0 + q < nbc ? __ldg(a.colsum + oq) : 0u;
         }
+        off += kFoldBatch * (stride - a.H) - a.H * (int64_t)(kFoldBatch * (kFoldBatch - 1) / 2);
+        stride -= kFoldBatch * a.H;
+      };
+      if (nbc > 0) load(0);
+      for (int64_t g0 = 0; g0 < nbc; g0 += kFoldBatch) {
+        uint32_t vv[kFoldBatch];
+#pragma unroll
+        for (int q = 0; q < kFoldBatch; ++q) vv[q] = vn[q];
+        if (g0 + kFoldBatch < nbc) load(g0 + kFoldBatch);
 #pragma unroll
         for (int q = 0; q < kFoldBatch; ++q) {
           if (g0 + q < nbc) {
@@ -191,8 +210,6 @@ __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, 
             lo += a.H;
           }
         }
-        off += kFoldBatch * (stride - a.H) - a.H * (int64_t)(kFoldBatch * (kFoldBatch - 1) / 2);
-        stride -= kFoldBatch * a.H;
       }
     }
     // row part: pieces of row c (only if the row belongs to these bands)
