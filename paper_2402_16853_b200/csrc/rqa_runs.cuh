@@ -109,22 +109,23 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 }
 
 // ---------------------------------------------------------------------------
-// Deferred run emission.  A pass over one word per lane only updates the
-// lane's run state (branch-free); the runs the word closes are described by
-// an event (boundary mask + the carried run) pushed into a per-warp ring in
-// shared memory, and events are expanded 32 at a time, one per lane, so the
-// histogram updates run at full SIMD width even when only a few lanes of a
-// pass see a boundary.
+// Deferred run emission.  A pass over one 64-bit word (two 32-bit words of a
+// sequence) per lane only updates the lane's run state (branch-free); the
+// runs the word closes are described by an event (64-bit boundary mask + the
+// carried run) pushed into a per-warp ring in shared memory, and events are
+// expanded 32 at a time, one per lane, so the histogram updates run at full
+// SIMD width even when only a few lanes of a pass see a boundary.
 // ---------------------------------------------------------------------------
-constexpr int kQueueCap = 256;  // events per warp (8 bytes each)
-// Drain when this many events are queued: every check follows at most 128
-// pushes (four words per lane), so the ring never holds more than 255.
-constexpr uint32_t kDrainAt = 128u;
+constexpr int kQueueCap = 128;  // events per warp (16 bytes each)
+// Drain when this many events are queued: every check follows at most 64
+// pushes (two 64-bit words per lane), so the ring never holds more than 127.
+constexpr uint32_t kDrainAt = 64u;
 
-// Event (8 bytes): x = boundary mask, y = carried run (len << 1 | bit) in
-// bits 0..28 plus flags in bits 29..31: bit 29 skip the carried run (it is
-// the sequence's first run, kept in the state), bits 30..31 diagonal weight
-// (0: vertical/white sink).  Runs are shorter than 2^28 (validate() bounds n).
+// Event (16 bytes): x, y = boundary mask (bits 0..31, 32..63), z = carried
+// run (len << 1 | bit) in bits 0..28 plus flags in bits 29..31: bit 29 skip
+// the carried run (it is the sequence's first run, kept in the state), bits
+// 30..31 diagonal weight (0: vertical/white sink).  Runs are shorter than 2^28
+// (validate() bounds n).
 constexpr uint32_t kEvCurBits = 29;
 constexpr uint32_t kEvCurMask = (1u << kEvCurBits) - 1u;
 // Shared word just past the histogram bins and the kernel's two mbarriers
@@ -142,24 +143,24 @@ __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint3
   if (!small && w) atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
 }
 
-__device__ __forceinline__ void expand_event(uint2 e, const Hist& h) {
-  uint32_t bnd = e.x;
-  const uint32_t flags = e.y >> kEvCurBits;
+__device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
+  unsigned long long bnd = ((unsigned long long)e.y << 32) | e.x;
+  const uint32_t flags = e.z >> kEvCurBits;
   const uint32_t w = flags >> 1;
-  const uint32_t ecur = e.y & kEvCurMask;
+  const uint32_t ecur = e.z & kEvCurMask;
   // weight and histogram row of runs of zeroes / ones
   const uint32_t w0 = (w == 0u) ? 1u : 0u, w1 = (w == 0u) ? 1u : w;
   const uint32_t k0 = kWhite, k1 = (w == 0u) ? (uint32_t)kVert : (uint32_t)kDiag;
   uint32_t bit = ecur & 1u;
   // first closed run: carried length + first boundary position
-  uint32_t p = (uint32_t)__ffs(bnd) - 1u;
+  uint32_t p = (uint32_t)__ffsll((long long)bnd) - 1u;
   uint32_t len = (ecur >> 1) + p;
   uint32_t wt = (flags & 1u) ? 0u : (bit ? w1 : w0);
   for (;;) {
     hist_red(h, bit ? k1 : k0, len, wt);  // wt == 0: predicated off
-    bnd &= bnd - 1u;
-    if (bnd == 0u) break;
-    const uint32_t q = (uint32_t)__ffs(bnd) - 1u;
+    bnd &= bnd - 1ull;
+    if (bnd == 0ull) break;
+    const uint32_t q = (uint32_t)__ffsll((long long)bnd) - 1u;
     len = q - p;
     p = q;
     bit ^= 1u;
@@ -168,7 +169,7 @@ __device__ __forceinline__ void expand_event(uint2 e, const Hist& h) {
 }
 
 struct EventQueue {
-  uint2* ring;       // this warp's kQueueCap entries
+  uint4* ring;       // this warp's kQueueCap entries
   uint32_t head;     // warp-uniform
   uint32_t tail;     // warp-uniform
   uint32_t lt_mask;  // (1 << lane) - 1
@@ -176,7 +177,7 @@ struct EventQueue {
 };
 
 // Expand whole groups of 32 events (all = true: everything left).  Kept out
-// of line: it runs once per ~10 passes and would otherwise be inlined at
+// of line: it runs once per few passes and would otherwise be inlined at
 // every pass site.
 static __device__ __noinline__ uint32_t queue_drain_impl(uint32_t ring_sa, uint32_t head,
                                                          uint32_t tail, uint32_t sh,
@@ -186,10 +187,10 @@ static __device__ __noinline__ uint32_t queue_drain_impl(uint32_t ring_sa, uint3
   while (tail - head >= 32u || (all && tail != head)) {
     const uint32_t avail = tail - head;
     if ((uint32_t)lane < avail) {
-      uint2 e;
-      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                   : "=r"(e.x), "=r"(e.y)
-                   : "r"(ring_sa + 8u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
+      uint4 e;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                   : "r"(ring_sa + 16u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
       expand_event(e, h);
     }
     head += avail < 32u ? avail : 32u;
@@ -203,23 +204,32 @@ __device__ __forceinline__ void queue_drain(EventQueue& q, const Hist& h, int la
   q.head = queue_drain_impl(q.ring_sa, q.head, q.tail, h.sh, h.g, h.stride, lane, all);
 }
 
-// One pass: consume nb (0..32) bits of x, bit 0 first, into the lane's run
-// state; closed runs go to the queue (no drain: the caller drains, the ring
-// holds kQueueCap events).  diag_weight 0: both run values count (vertical /
+__device__ __forceinline__ void queue_check(EventQueue& q, const Hist& h, int lane) {
+  if (q.tail - q.head >= kDrainAt) queue_drain(q, h, lane, false);
+}
+
+// One pass: consume nb (0..64) bits of lo | hi << 32, bit 0 first, into the
+// lane's run state; closed runs go to the queue (no drain: the caller drains
+// after at most two passes).  diag_weight 0: both run values count (vertical /
 // white vertical); 1 or 2: only runs of ones count as diagonal lines with
 // that weight.  All lanes of the warp must call it (nb = 0 for lanes with
 // nothing to consume).  Branch-free.
-__device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
-                                          EventQueue& q) {
-  const uint32_t full = (nb >= 32) ? 0xffffffffu : ((1u << nb) - 1u);
-  x &= full;
-  const uint32_t cur = st.cur ? st.cur : (x & 1u);            // sequence starts here
-  const uint32_t bnd = (x ^ ((x << 1) | (cur & 1u))) & full;  // run boundaries
-  const bool ev = bnd != 0u;
-  const uint32_t plast = 31u - (uint32_t)__clz(bnd);           // last boundary
-  const uint32_t p1 = (uint32_t)__ffs(bnd) - 1u;               // first boundary
-  const bool mkfirst = ev && st.first == 0u;                   // carried run is the first run
-  const uint32_t cur_ev = (((uint32_t)nb - plast) << 1) | ((x >> (plast & 31u)) & 1u);
+__device__ __forceinline__ void runs_push(uint32_t lo, uint32_t hi, int nb, RunState& st,
+                                          uint32_t diag_weight, EventQueue& q) {
+  const uint32_t flo = (nb >= 32) ? 0xffffffffu : ((1u << nb) - 1u);
+  const uint32_t fhi = (nb >= 64) ? 0xffffffffu : (nb > 32 ? ((1u << (nb - 32)) - 1u) : 0u);
+  lo &= flo;
+  hi &= fhi;
+  const uint32_t cur = st.cur ? st.cur : (lo & 1u);                   // sequence starts here
+  const uint32_t blo = (lo ^ ((lo << 1) | (cur & 1u))) & flo;          // run boundaries
+  const uint32_t bhi = (hi ^ __funnelshift_l(lo, hi, 1)) & fhi;
+  const bool ev = (blo | bhi) != 0u;
+  const uint32_t plast = bhi ? 63u - (uint32_t)__clz(bhi) : 31u - (uint32_t)__clz(blo);
+  const uint32_t p1 = blo ? (uint32_t)__ffs(blo) - 1u : 31u + (uint32_t)__ffs(bhi);
+  // the last run's bit is the last consumed bit
+  const uint32_t lastbit = (nb > 32 ? hi >> ((uint32_t)(nb - 33) & 31u) : lo >> ((uint32_t)(nb - 1) & 31u)) & 1u;
+  const bool mkfirst = ev && st.first == 0u;                          // carried run is the first run
+  const uint32_t cur_ev = (((uint32_t)nb - plast) << 1) | lastbit;
   st.first = mkfirst ? cur + (p1 << 1) : st.first;
   st.cur = ev ? cur_ev : cur + ((uint32_t)nb << 1);
   const uint32_t m = __ballot_sync(0xffffffffu, ev);
@@ -227,17 +237,11 @@ __device__ __forceinline__ void runs_push(uint32_t x, int nb, RunState& st, uint
   // no generic-address rematerialisation per push
   const uint32_t slot = (q.tail + __popc(m & q.lt_mask)) & (uint32_t)(kQueueCap - 1);
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
-      "@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(q.ring_sa + 8u * slot),
-      "r"(bnd), "r"(cur | (((diag_weight << 1) | (mkfirst ? 1u : 0u)) << kEvCurBits)),
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@p st.shared.v4.u32 [%0], {%1, %2, %3, %3};\n\t}" ::"r"(q.ring_sa + 16u * slot),
+      "r"(blo), "r"(bhi), "r"(cur | (((diag_weight << 1) | (mkfirst ? 1u : 0u)) << kEvCurBits)),
       "r"(ev ? 1u : 0u));  // no memory clobber: the ring is only accessed through asm
   q.tail += __popc(m);
-}
-
-__device__ __forceinline__ void runs_pass(uint32_t x, int nb, RunState& st, uint32_t diag_weight,
-                                          EventQueue& q, const Hist& h, int lane) {
-  runs_push(x, nb, st, diag_weight, q);
-  if (q.tail - q.head >= kDrainAt) queue_drain(q, h, lane, false);
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {

@@ -101,8 +101,8 @@ struct SymSmem {
     off_prev = off_rowbuf + (size_t)NW * H * sizeof(uint32_t);
     off_colst = off_prev + 2 * (size_t)H * sizeof(uint32_t);
     off_rowst = off_colst + (size_t)NW * R * 32 * sizeof(uint2);
-    off_queue = off_rowst + (size_t)R * D * sizeof(uint2);
-    off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint2);
+    off_queue = (off_rowst + (size_t)R * D * sizeof(uint2) + 15) & ~(size_t)15;  // 16-B events
+    off_hist = off_queue + (size_t)NW * kQueueCap * sizeof(uint4);
     // bins, two mbarriers (16 B), the dummy bin of hist_red (16 B reserved)
     off_cand = off_hist + 3 * kSmemBins * sizeof(uint32_t) + 32;
     off_cres = off_cand + (size_t)NW * cand_cap * sizeof(uint16_t);

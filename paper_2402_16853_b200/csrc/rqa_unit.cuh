@@ -201,7 +201,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   uint32_t rowbuf_sa = smem_u32(rowbuf + wv * H + lane);
   int skip = a.skip;
   asm volatile("" : "+r"(rowbuf_sa), "+r"(skip));
-  EventQueue evq{reinterpret_cast<uint2*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
+  EventQueue evq{reinterpret_cast<uint4*>(smem + L.off_queue) + wv * kQueueCap, 0u, 0u,
                  (1u << lane) - 1u};
   evq.ring_sa = smem_u32(evq.ring);
   uint16_t* Pb = a.P + band_offset(b, n, a.row_lo, H);  // band-level diagonal summaries
@@ -341,10 +341,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         fullmask |= 1u << r;
 
     // the R words of chunk c are final: their transposed row words go to
-    // rowbuf (the R transposes are independent and interleave), then the
-    // diagonal runs of their 32 rows; one drain check after the R <= 4
-    // pushes (<= 127 queued + 4 x 32 pushed < kQueueCap)
-    auto finish_chunk = [&](int c, uint32_t (&w)[R]) {
+    // rowbuf (the R transposes are independent and interleave)
+    auto chunk_rows = [&](int c, uint32_t (&w)[R]) {
       uint32_t tw[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -353,21 +351,26 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) rowbuf[wv * H + r * HS + 32 * c + lane] = tw[r];
+    };
+    // diagonal runs of chunks c and c+1 (64 rows per slot); one drain check
+    // after every two pushes (<= 63 queued + 2 x 32 pushed < kQueueCap)
+    auto diag_pass = [&](int c, const uint32_t (&w0)[R], const uint32_t (&w1)[R]) {
       if (warm || (skip & 1)) return;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int kd = kdr[r];
         if ((fullmask >> r) & 1u) {
-          runs_push(w[r], 32, st[r], kd == 0 ? 1u : 2u, evq);
+          runs_push(w0[r], w1[r], 64, st[r], kd == 0 ? 1u : 2u, evq);
         } else {
           // past the diagonal's last row (matrix edge) nothing is consumed;
           // the piece is closed at the end of the iteration
           const bool live = kd >= 0 && kd < nrem;
           const int rel = lastc[r] - 32 * c;
-          runs_push(w[r], live ? min(max(rel, 0), 32) : 0, st[r], kd == 0 ? 1u : 2u, evq);
+          runs_push(w0[r], w1[r], live ? min(max(rel, 0), 64) : 0, st[r], kd == 0 ? 1u : 2u, evq);
         }
+        if (r & 1) queue_check(evq, hist, lane);
       }
-      if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+      if (R & 1) queue_check(evq, hist, lane);
     };
 
     if constexpr (kPre) {
@@ -568,14 +571,21 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
         __syncthreads();  // resolved words visible to their owners
       }
-      // ---- phase 2: final words -> diagonal runs, transposed row words
-      for (int c = 0; c < NCH; ++c) {
-        uint32_t w[R];
+      // ---- phase 2: final words -> transposed row words, diagonal runs
+      static_assert(NCH % 2 == 0, "chunk pairs");
+      for (int c = 0; c < NCH; c += 2) {
+        uint32_t w0[R], w1[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) w[r] = lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c));
-        finish_chunk(c, w);
+        for (int r = 0; r < R; ++r) {
+          w0[r] = lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c));
+          w1[r] = lds_u32(rowbuf_sa + 4u * (uint32_t)(r * HS + 32 * c + 32));
+        }
+        chunk_rows(c, w0);
+        chunk_rows(c + 1, w1);
+        diag_pass(c, w0, w1);
       }
-    } else
+    } else {
+    uint32_t wprev[R];  // words of the even chunk of a pair (diagonal runs per chunk pair)
     for (int c = 0; c < NCH; ++c) {
       uint32_t dw[R];
       float amb[R];  // f32 filter: min |acc32 - c32| over the word (per pair when packed)
@@ -728,7 +738,14 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           words[r] = dw[r];
         }
       }
-      finish_chunk(c, words);
+      chunk_rows(c, words);
+      if (c & 1) {
+        diag_pass(c - 1, wprev, words);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) wprev[r] = words[r];
+      }
+    }
     }
     __syncthreads();
 
@@ -758,31 +775,29 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           rs[p] = RunState{rsv.x, rsv.y};
         }
         if (__all_sync(0xffffffffu, all_full)) {
-          static_assert(NW % 2 == 0 && PR <= 2, "row phase: 2 x PR pushes per drain check");
+          static_assert(NW % 2 == 0 && PR <= 2, "row phase: PR pushes of 64 bits per drain check");
 #pragma unroll 1
           for (int v = 0; v < NW; v += 2) {
 #pragma unroll
-            for (int vv = 0; vv < 2; ++vv) {
-#pragma unroll
-              for (int p = 0; p < PR; ++p) {
-                const uint32_t w = rowbuf[(v + vv) * H + lr[p]];
-                pts += __popc(w);
-                runs_push(w, 32, rs[p], 0u, evq);
-              }
+            for (int p = 0; p < PR; ++p) {
+              const uint32_t w0 = rowbuf[v * H + lr[p]], w1 = rowbuf[(v + 1) * H + lr[p]];
+              pts += __popc(w0) + __popc(w1);
+              runs_push(w0, w1, 64, rs[p], 0u, evq);
             }
-            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+            queue_check(evq, hist, lane);
           }
         } else {
 #pragma unroll 1
-          for (int v = 0; v < NW; ++v) {
+          for (int v = 0; v < NW; v += 2) {
 #pragma unroll
             for (int p = 0; p < PR; ++p) {
-              const int nb = min(max(rem[p] - 32 * v, 0), 32);
-              const uint32_t w = rowbuf[v * H + lr[p]] & low_mask(nb);
-              pts += __popc(w);
-              runs_push(w, nb, rs[p], 0u, evq);
+              const int nb = min(max(rem[p] - 32 * v, 0), 64);
+              const uint32_t w0 = rowbuf[v * H + lr[p]] & low_mask(nb);
+              const uint32_t w1 = rowbuf[(v + 1) * H + lr[p]] & (nb > 32 ? low_mask(nb - 32) : 0u);
+              pts += __popc(w0) + __popc(w1);
+              runs_push(w0, w1, nb, rs[p], 0u, evq);
             }
-            if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
+            queue_check(evq, hist, lane);
           }
         }
 #pragma unroll
@@ -821,37 +836,41 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
         if (!(skip & 4) && x >= rs_[PR - 1]) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
-          // shifted into aligned columns, transposed, met bottom-up
-          auto col_step = [&](int c, const int* lim, auto full) {
+          // shifted into aligned columns, transposed, bit-reversed (columns
+          // are met bottom-up); all lanes take part (transpose)
+          auto col_word = [&](int c, int p) {
             const int wp = (wv - c) & (NW - 1);
+            const int lrow = rs_[p] * HS + 32 * c + lane;
+            const uint32_t w1 = rowbuf[wp * H + lrow];
+            const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
+            return __brev(tr(__funnelshift_l(w0, w1, lane)));
+          };
+          // windows c and c-1 (c-1 < lo: none) as one 64-bit pass per slot;
+          // partial columns keep the rows below lim (a window's valid rows are
+          // its top ones: after the bit reversal, its high bits)
+          auto col_pair = [&](int c, int lo, const int* lim, auto full) {
 #pragma unroll
             for (int p = 0; p < PR; ++p) {
-              const int lrow = rs_[p] * HS + 32 * c + lane;
-              const uint32_t w1 = rowbuf[wp * H + lrow];
-              const uint32_t w0 = wp > 0 ? rowbuf[(wp - 1) * H + lrow] : prev_cur[lrow];
-              const uint32_t colw = tr(__funnelshift_l(w0, w1, lane));
-              if constexpr (decltype(full)::value) {  // every lane: 32 rows of the column
-                runs_push(__brev(colw), 32, cur[p], 0u, evq);
+              const uint32_t a0 = col_word(c, p);
+              const uint32_t a1 = c - 1 >= lo ? col_word(c - 1, p) : 0u;
+              if constexpr (decltype(full)::value) {  // every lane: 32 rows per window
+                runs_push(a0, a1, c - 1 >= lo ? 64 : 32, cur[p], 0u, evq);
               } else {
-                const int nb = min(max(lim[p] - 32 * c, 0), 32);
-                const uint32_t bits = __funnelshift_rc(__brev(colw), 0u, 32 - nb);
-                runs_push(bits, nb, cur[p], 0u, evq);
+                const int n0 = min(max(lim[p] - 32 * c, 0), 32);
+                const int n1 = c - 1 >= lo ? min(max(lim[p] - 32 * (c - 1), 0), 32) : 0;
+                const uint32_t b0 = __funnelshift_rc(a0, 0u, 32 - n0);
+                const uint32_t b1 = __funnelshift_rc(a1, 0u, 32 - n1);
+                const unsigned long long x64 = (unsigned long long)b0 |
+                                               ((unsigned long long)b1 << n0);
+                runs_push((uint32_t)x64, (uint32_t)(x64 >> 32), n0 + n1, cur[p], 0u, evq);
               }
             }
+            queue_check(evq, hist, lane);
           };
-          // windows c = hi, hi-1, ..., lo (descending), two per drain check
+          // windows c = hi, hi-1, ..., lo (descending), two per pass
           auto col_steps = [&](int hi, int lo, const int* lim, auto full) {
-            int c = hi;
 #pragma unroll 1
-            for (; c - 1 >= lo; c -= 2) {
-              col_step(c, lim, full);
-              col_step(c - 1, lim, full);
-              if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
-            }
-            if (c >= lo) {
-              col_step(c, lim, full);
-              if (evq.tail - evq.head >= kDrainAt) queue_drain(evq, hist, lane, false);
-            }
+            for (int c = hi; c >= lo; c -= 2) col_pair(c, lo, lim, full);
           };
           using kFull = std::integral_constant<bool, true>;
           using kPart = std::integral_constant<bool, false>;
