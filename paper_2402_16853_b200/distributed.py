@@ -5,7 +5,7 @@ on band boundaries.  Rows never cross stripes, so vertical and white-vertical
 lines (row runs, by R = R^T) are complete on each rank; only diagonal lines
 cross stripe edges.  Each rank reports, per diagonal k >= 0, the 1-run
 starting at its top edge and ending at its bottom edge; rank 0 gathers those
-(all_gather over NCCL / NVLink), folds them in row order with the carry
+(gather over NCCL / NVLink), folds them in row order with the carry
 contract of engine.py:287-319 and adds the crossing runs; histograms are
 summed with a reduce.  torch.distributed is plumbing; the compute is
 librqa_b200.so.
@@ -90,29 +90,37 @@ def all_reduce(t, op=None, group=None):
         _gloo_staged(lambda h: dist.all_reduce(h, op=op, group=group), t)
 
 
-def exchange(so, world, group=None):
-    """All-gather the stripe edge summaries, sum the row leads (disjoint rows)."""
+def exchange(so, world, group=None, dst=0):
+    """Gather the stripe edge summaries on rank ``dst`` (the only rank that
+    stitches) and sum the row parts there (disjoint rows).  Returns the
+    gathered StripeOutputs on ``dst``, None elsewhere."""
     import torch
     import torch.distributed as dist
 
     from .device import StripeOutputs
 
+    rank = dist.get_rank(group)
     n = so.prefix.numel()
     dev = so.prefix.device
-    out = StripeOutputs(torch.empty(world, n, dtype=so.prefix.dtype, device=dev),
-                        torch.empty(world, n, dtype=so.suffix.dtype, device=dev),
-                        torch.empty(world, 2 * n, dtype=so.col.dtype, device=dev),
-                        so.rowlead)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out.prefix, so.prefix, group=group)
-        dist.all_gather_into_tensor(out.suffix, so.suffix, group=group)
-        dist.all_gather_into_tensor(out.col, so.col, group=group)
-    else:  # gloo (CPU tests / shared-GPU test runs): list form on host copies
-        for dst, src in ((out.prefix, so.prefix), (out.suffix, so.suffix), (out.col, so.col)):
-            parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
-            dist.all_gather(parts, src.cpu(), group=group)
-            dst.copy_(torch.stack(parts))
-    all_reduce(out.rowlead, group=group)
+    out = None
+    if rank == dst:
+        out = StripeOutputs(torch.empty(world, n, dtype=so.prefix.dtype, device=dev),
+                            torch.empty(world, n, dtype=so.suffix.dtype, device=dev),
+                            torch.empty(world, 2 * n, dtype=so.col.dtype, device=dev),
+                            so.rowlead)
+    nccl = dist.get_backend(group) == "nccl"
+    for name in ("prefix", "suffix", "col"):
+        src = getattr(so, name)
+        if nccl:
+            parts = list(getattr(out, name).unbind(0)) if rank == dst else None
+            dist.gather(src, gather_list=parts, dst=dst, group=group)
+        else:  # gloo (CPU tests / shared-GPU test runs): host copies
+            parts = [torch.empty_like(src, device="cpu") for _ in range(world)] \
+                if rank == dst else None
+            dist.gather(src.cpu(), gather_list=parts, dst=dst, group=group)
+            if rank == dst:
+                getattr(out, name).copy_(torch.stack(parts))
+    reduce_sum(so.rowlead, dst, group)
     return out
 
 
