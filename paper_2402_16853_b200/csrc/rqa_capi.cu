@@ -126,7 +126,28 @@ struct Workspace {
   size_t bins_cap = 0;
   cudaEvent_t ev[6] = {};
   bool init = false;
+  unsigned long long* host_stats = nullptr;  // pinned [4]: f32 stats + sampled hits (one D2H)
+  // last unit plan uploaded (reused while the geometry is unchanged: no
+  // host planning or H2D copy inside repeated runs)
+  int64_t plan_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  int64_t plan_nunits = 0;
 };
+
+// Resident CTAs per SM of a kernel variant (queried once per kernel).
+int variant_occupancy(const Variant& v, int* per_sm) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& e : cache)
+    if (e.first == v.kernel) return *per_sm = e.second, 0;
+  cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)v.smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, v.kernel, 32 * v.nw, v.smem);
+  if (e != cudaSuccess) return (int)e;
+  cache.emplace_back(v.kernel, *per_sm);
+  return 0;
+}
 
 std::mutex g_ws_mu;
 std::vector<Workspace*> g_ws;        // [slot * kMaxDevices + device]
@@ -450,29 +471,44 @@ int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
   if (want != 1 && p->n < ((int64_t)1 << 15)) return RQA_OK;
   const double dstar = prefilter_bound(p->metric, p->thr);
   if (!(dstar >= 0) || std::isinf(dstar)) return RQA_OK;
-  if (want != 1) {
-    const int samples = 1 << 16;
-    RQA_CUDA(grow(&ws->maxbits, &ws->maxbits_cap, 2), "allocating");
-    RQA_CUDA(cudaMemsetAsync(ws->maxbits + 1, 0, sizeof(unsigned long long), st), "memset");
+  // one device round trip: the sampled candidate fraction (decides the
+  // kernel) and, for the packed float32 predicate, max |s| of the staged
+  // float32 series (bounds the predicate)
+  const bool sample = want != 1;
+  const int samples = 1 << 16;
+  RQA_CUDA(grow(&ws->stats, &ws->stats_cap, 3), "allocating");
+  if (!ws->host_stats)
+    RQA_CUDA(cudaMallocHost(&ws->host_stats, 4 * sizeof(unsigned long long)), "allocating");
+  RQA_CUDA(cudaMemsetAsync(ws->stats, 0, 3 * sizeof(unsigned long long), st), "memset");
+  if (pv.f32pred) {
+    const size_t count = (size_t)(p->len + 2 * p->pad);
+    RQA_CUDA(grow(&ws->sf_pad, &ws->sf_cap, count), "allocating float32 series");
+    prep_f32_kernel<<<148 * 4, 256, 0, st>>>(ws->s_pad, ws->sf_pad, (int64_t)count, ws->stats);
+    RQA_CUDA(cudaGetLastError(), "launching f32 staging");
+    g_launches++;
+    p->sf = ws->sf_pad + p->pad;
+  }
+  if (sample) {
     sample_candidates_kernel<<<samples / 256, 256, 0, st>>>(ws->s_pad + p->pad, p->n, p->m,
                                                            p->tau, dstar, samples,
-                                                           ws->maxbits + 1);
+                                                           ws->stats + 2);
     RQA_CUDA(cudaGetLastError(), "launching candidate sampling");
     g_launches++;
-    unsigned long long hits = 0;
-    RQA_CUDA(cudaMemcpyAsync(&hits, ws->maxbits + 1, sizeof hits, cudaMemcpyDeviceToHost, st),
+  }
+  if (sample || pv.f32pred) {
+    RQA_CUDA(cudaMemcpyAsync(ws->host_stats, ws->stats, 3 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st),
              "d2h");
-    RQA_CUDA(cudaStreamSynchronize(st), "candidate sampling");
-    p->cand = (double)hits / samples;
+    RQA_CUDA(cudaStreamSynchronize(st), "prefilter planning");
+  }
+  if (sample) {
+    p->cand = (double)ws->host_stats[2] / samples;
     if (p->cand > prefilter_max(p->m)) return RQA_OK;
   }
   if (pv.f32pred) {
     double maxabs = 0.0;
-    bool finite = false;
-    int rc = stage_f32(ws, p, st, &maxabs, &finite, err, errlen);
-    if (rc) return rc;
+    memcpy(&maxabs, &ws->host_stats[0], sizeof maxabs);
     float d2 = 0.f;
-    (void)finite;
     if (!prefilter_f32_bound(dstar, maxabs, &d2)) return RQA_OK;
     p->pre_negd2 = -d2;
   }
@@ -553,33 +589,37 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  RQA_CUDA(cudaFuncSetAttribute(p.var.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)p.var.smem),
-           "kernel attributes");
-  RQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.var.kernel, 32 * p.var.nw,
-                                                         p.var.smem),
-           "occupancy");
-  const UnitPlan pl = plan_units(p, row_lo, row_hi, sms * std::max(1, per_sm));
-  const int64_t nunits = (int64_t)pl.units.size();
-  const int64_t ctot = sym_band_offset(nb, p.n, row_lo, H);
+  if (int e = variant_occupancy(p.var, &per_sm)) return cuda_fail((cudaError_t)e, "occupancy", err, errlen);
+  const int slots = sms * std::max(1, per_sm);
   const int64_t D = p.var.slot_rows(), R = p.var.r;
+  const int64_t key[8] = {p.n, row_lo, row_hi, H, D, R, slots, (int64_t)p.var.nw};
+  int64_t nunits = ws->plan_nunits;
+  if (!std::equal(key, key + 8, ws->plan_key)) {
+    // a new geometry: plan, upload (ordered on st before the kernel), remember
+    const UnitPlan pl = plan_units(p, row_lo, row_hi, slots);
+    nunits = (int64_t)pl.units.size();
+    RQA_CUDA(grow(&ws->units, &ws->units_cap, (size_t)nunits), "allocating units");
+    RQA_CUDA(grow(&ws->units_bb, &ws->units_bb_cap, (size_t)nunits), "allocating units");
+    RQA_CUDA(grow(&ws->band_start, &ws->band_start_cap, (size_t)nb + 1), "allocating units");
+    RQA_CUDA(cudaMemcpyAsync(ws->units, pl.units.data(), nunits * sizeof(Unit),
+                             cudaMemcpyHostToDevice, st),
+             "copying units");
+    RQA_CUDA(cudaMemcpyAsync(ws->units_bb, pl.by_band.data(), nunits * sizeof(int4),
+                             cudaMemcpyHostToDevice, st),
+             "copying units");
+    RQA_CUDA(cudaMemcpyAsync(ws->band_start, pl.band_start.data(), (nb + 1) * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, st),
+             "copying units");
+    RQA_CUDA(cudaStreamSynchronize(st), "copying units");  // pageable sources go out of scope
+    std::copy(key, key + 8, ws->plan_key);
+    ws->plan_nunits = nunits;
+  }
+  const int64_t ctot = sym_band_offset(nb, p.n, row_lo, H);
   RQA_CUDA(grow(&ws->ps, &ws->ps_cap, (size_t)(2 * ctot)), "allocating diagonal summaries");
   RQA_CUDA(grow(&ws->drec, &ws->drec_cap, (size_t)(nunits * std::max<int64_t>(R - 1, 1) * D)),
            "allocating diagonal records");
   RQA_CUDA(grow(&ws->cs, &ws->cs_cap, (size_t)ctot), "allocating column summaries");
   RQA_CUDA(grow(&ws->rowpiece, &ws->rowpiece_cap, (size_t)(nunits * H)), "allocating row pieces");
-  RQA_CUDA(grow(&ws->units, &ws->units_cap, (size_t)nunits), "allocating units");
-  RQA_CUDA(grow(&ws->units_bb, &ws->units_bb_cap, (size_t)nunits), "allocating units");
-  RQA_CUDA(grow(&ws->band_start, &ws->band_start_cap, (size_t)nb + 1), "allocating units");
-  RQA_CUDA(cudaMemcpyAsync(ws->units, pl.units.data(), nunits * sizeof(Unit),
-                           cudaMemcpyHostToDevice, st),
-           "copying units");
-  RQA_CUDA(cudaMemcpyAsync(ws->units_bb, pl.by_band.data(), nunits * sizeof(int4),
-                           cudaMemcpyHostToDevice, st),
-           "copying units");
-  RQA_CUDA(cudaMemcpyAsync(ws->band_start, pl.band_start.data(), (nb + 1) * sizeof(int32_t),
-                           cudaMemcpyHostToDevice, st),
-           "copying units");
   uint32_t* rowpart = out_row;
   if (!rowpart) {  // final mode: the hook fold does not need a separate row-part array
     RQA_CUDA(grow(&ws->rowlead, &ws->rowlead_cap, (size_t)(2 * p.n)), "allocating row parts");
@@ -724,12 +764,14 @@ std::vector<int64_t> area_stripes(int64_t n, int g, int64_t band) {
 // code path as multi-GPU) when the summaries would not fit in memory.
 int run_full(Workspace* ws, const Problem& p, unsigned long long* hist, unsigned long long* points,
              cudaStream_t st, cudaEvent_t ev_mid, char* err, size_t errlen) {
-  size_t free_b = 0, total_b = 0;
-  RQA_CUDA(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-  const double budget = 0.6 * (double)(free_b + ws->ps_cap * 2 + ws->cs_cap * 4);
   const double need = (double)unit_workspace_bytes(p, 0, p.n);
   int g = 1;
-  while (need / g > budget && g < 64) g *= 2;
+  if (need > (double)(ws->ps_cap * 2 + ws->cs_cap * 4)) {  // buffers must grow: check memory
+    size_t free_b = 0, total_b = 0;
+    RQA_CUDA(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const double budget = 0.6 * (double)(free_b + ws->ps_cap * 2 + ws->cs_cap * 4);
+    while (need / g > budget && g < 64) g *= 2;
+  }
   if (g == 1)
     return launch_rows(ws, p, 0, p.n, kFoldFinal, hist, points, nullptr, nullptr, nullptr, nullptr,
                        st, ev_mid, err, errlen);
@@ -1252,6 +1294,7 @@ int rqa_release(void) {
     cudaFree(ws->sf_pad);
     cudaFree(ws->maxbits);
     cudaFree(ws->stats);
+    if (ws->host_stats) cudaFreeHost(ws->host_stats);
     cudaFree(ws->ps);
     cudaFree(ws->cs);
     cudaFree(ws->rowlead);
