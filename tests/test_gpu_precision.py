@@ -160,9 +160,19 @@ for kind, m, tau, metric, r, w in (("uniform", 3, 1, "l2", 0.1, 0), ("uniform", 
                                    ("sine", 2, 1, "l2", 0.5, 0), ("uniform", 5, 1, "l2", 0.3, 2),
                                    ("uniform", 3, 1, "l1", 0.2, 0), ("sine", 2, 2, "l1", 1.0, 0),
                                    ("uniform", 4, 2, "l2", 0.25, 0), ("sine", 10, 5, "l1", 3.0, 10),
-                                   ("sine", 5, 5, "l2", 0.8, 1)):
+                                   ("sine", 5, 5, "l2", 0.8, 1),
+                                   # long windows use the component-PAIR predicate: ties at
+                                   # the radius on integer data, dense and sparse radii
+                                   ("grid", 10, 5, "l1", 4.0, 0), ("grid", 5, 5, "l2", 3.0, 0),
+                                   ("grid", 10, 5, "l2", 6.0, 3), ("sine", 5, 5, "l1", 2.5, 0),
+                                   ("uniform", 10, 5, "l1", 1.5, 0)):
     n = 3100
-    s = rng.uniform(0, 1, n) if kind == "uniform" else np.sin(np.linspace(0, 60, n)) + 0.1 * rng.normal(size=n)
+    if kind == "uniform":
+        s = rng.uniform(0, 1, n)
+    elif kind == "grid":
+        s = rng.integers(0, 3, n).astype(np.float64)
+    else:
+        s = np.sin(np.linspace(0, 60, n)) + 0.1 * rng.normal(size=n)
     s[100] = np.nan
     h, t = run_analysis(embed(s, m, tau), AnalysisSettings(m, tau, metric, r, theiler_corrector=w))
     d, v, wh, p = oracle_histograms(s, m, tau, metric, r, w, tile_size=512)
