@@ -44,11 +44,15 @@ def ops_per_cell(settings) -> int:
 def executed_ops_per_cell(settings, evaluation="fp64", candidates=None) -> float:
     """FP64 ops per evaluated cell the chosen kernel issues.
 
-    fp64: term reuse (App. A.3/A.4); fp64-prefilter: DADD + DSETP per cell
-    plus the full 3m (L2) / 2m (L1) sum for the sampled candidate fraction."""
+    fp64: term reuse (App. A.3/A.4); fp64-prefilter: for m <= 4 the component
+    predicate runs in packed float32 (no FP64), for m >= 5 the pair predicate
+    issues 2 DADD + DADD + DSETP (+ 2 DMUL for L2) per cell; plus the full
+    3m (L2) / 2m (L1) sum for the sampled candidate fraction (the component
+    fraction, an upper bound for the pair predicate)."""
     m = settings.embedding_dimension
     if evaluation == "fp64-prefilter" and candidates is not None and candidates >= 0:
-        return 2 + candidates * ops_per_cell(settings)
+        per_cell = 0 if m <= 4 else (4 if settings.metric == "l1" else 6)
+        return per_cell + candidates * ops_per_cell(settings)
     if m == 1 or settings.metric == "linf":
         return 2
     return m + 2 if settings.metric == "l2" else m + 1

@@ -8,10 +8,11 @@ import sys
 
 rep = sys.argv[1]
 src = open("paper_2402_16853_b200/csrc/rqa_unit.cuh").read().splitlines()
-marks = [("finish_chunk", "auto finish_chunk"), ("phase1", "if constexpr (kPre) {"),
-         ("phase2", "// ---- phase 2"), ("generic eval", "    for (int c = 0; c < NCH; ++c) {\n"),
+marks = [("chunk_rows", "auto chunk_rows"), ("diag_pass", "auto diag_pass"),
+         ("phase1 (predicate + candidates)", "if constexpr (kPre) {"),
+         ("phase2", "// ---- phase 2"), ("generic eval", "uint32_t wprev[R];"),
          ("row phase", "// ---- row phase"), ("column phase", "// ---- column phase"),
-         ("diag end", "// ---- every slot's diagonal"), ("tail", "// ---- row pieces")]
+         ("diag end", "// ---- diagonal pieces"), ("tail", "// ---- row pieces")]
 starts = []
 for name, m in marks:
     for i, line in enumerate(src):
