@@ -699,8 +699,7 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   f.hist = hist;
   f.out_p = out_p;
   f.out_s = out_s;
-  sym_fold_diag<<<(int)blocks, threads, 0, st>>>(f, mode);
-  RQA_CUDA(cudaGetLastError(), "launching diagonal fold");
+
   UnitFoldArgs h;
   memset(&h, 0, sizeof h);
   h.colsum = ws->cs;
@@ -717,9 +716,14 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   h.hist = hist;
   h.out_col = reinterpret_cast<uint2*>(out_col);
   h.out_row = reinterpret_cast<uint2*>(rowpart);
-  unit_fold_hooks<<<(int)blocks, threads, 0, st>>>(h, mode);
-  RQA_CUDA(cudaGetLastError(), "launching hook fold");
-  g_launches += 2;
+  // one launch: the diagonal fold (about a fifth of the fold time) and the
+  // hook fold share the grid
+  static const char* dfrac = getenv("RQA_FOLD_DIAG_SHARE");
+  const double share = dfrac ? atof(dfrac) : 0.3;
+  const int dblocks = (int)std::max<int64_t>(1, (int64_t)(blocks * share));
+  unit_fold_all<<<(int)blocks + dblocks, threads, 0, st>>>(f, h, mode, dblocks);
+  RQA_CUDA(cudaGetLastError(), "launching folds");
+  g_launches += 1;
   return RQA_OK;
 }
 

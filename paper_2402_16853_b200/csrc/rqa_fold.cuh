@@ -67,16 +67,18 @@ __host__ __device__ __forceinline__ int64_t sym_band_offset(int64_t b, int64_t n
 // Diagonal k >= 0 folded over the segments (height H) of [row_lo, row_hi);
 // mode: kFoldFinal counts every run, kFoldStripe reports the runs touching
 // the stripe's top / bottom edges.  Offsets advance incrementally (compact layout).
-__global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, const int mode) {
+// Body of the diagonal fold for block `bid` of `nblk` (the fused fold kernel
+// runs it next to the hook fold; bins: the block's shared histogram).
+__device__ __forceinline__ void fold_diag_body(const SymFoldArgs& a, const int mode, int64_t bid,
+                                               int64_t nblk, uint32_t* bins) {
   const int64_t n = a.n;
-  __shared__ uint32_t bins[3 * kSmemBins];
   FoldBins fb{bins};
   fb.init();
   const Hist h{smem_u32(bins), a.hist, n + 1};
   // a thread folds diagonals t and n-1-t: their segment counts add up to
   // about the same for every thread (the upper triangle is balanced)
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
-       t += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t t = bid * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
+       t += nblk * blockDim.x)
   for (int side = 0; side < 2; ++side) {
     const int64_t k = side ? n - 1 - t : t;
     if (side && k == t) break;
@@ -137,6 +139,11 @@ __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, con
   fb.flush(a.hist, n);
 }
 
+__global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, const int mode) {
+  __shared__ uint32_t bins[3 * kSmemBins];
+  fold_diag_body(a, mode, blockIdx.x, gridDim.x, bins);
+}
+
 }  // namespace rqa
 
 // ===========================================================================
@@ -159,15 +166,15 @@ struct UnitFoldArgs {
   uint2* out_row;              // stripe mode: row part per row (rows of the stripe)
 };
 
-__global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, const int mode) {
+__device__ __forceinline__ void fold_hooks_body(const UnitFoldArgs& a, const int mode,
+                                                int64_t bid, int64_t nblk, uint32_t* bins) {
   const int64_t n = a.n;
-  __shared__ uint32_t bins[3 * kSmemBins];
   FoldBins fb{bins};
   fb.init();
   const Hist h{smem_u32(bins), a.hist, n + 1};
   // a thread folds hooks t and n-1-t (balanced band counts, as sym_fold_diag)
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
-       t += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t t = bid * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
+       t += nblk * blockDim.x)
   for (int side = 0; side < 2; ++side) {
     const int64_t c = side ? n - 1 - t : t;
     if (side && c == t) break;
@@ -238,6 +245,23 @@ __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, 
   }
   fb.flush(a.hist, n);
 }
+
+__global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, const int mode) {
+  __shared__ uint32_t bins[3 * kSmemBins];
+  fold_hooks_body(a, mode, blockIdx.x, gridDim.x, bins);
+}
+
+// Both folds in one launch: blocks [0, diag_blocks) fold diagonals, the rest
+// fold hooks (independent inputs; the two latency-bound folds overlap).
+__global__ void __launch_bounds__(256, 4) unit_fold_all(const SymFoldArgs d, const UnitFoldArgs u,
+                                                        const int mode, const int diag_blocks) {
+  __shared__ uint32_t bins[3 * kSmemBins];
+  if ((int)blockIdx.x < diag_blocks)
+    fold_diag_body(d, mode, blockIdx.x, diag_blocks, bins);
+  else
+    fold_hooks_body(u, mode, blockIdx.x - diag_blocks, gridDim.x - diag_blocks, bins);
+}
+
 
 // Diagonal band segments cut by a work-unit boundary (rqa_unit.cuh): unit u
 // walked the upper part (slots 0..rA, open at the cut) and unit u+1 of the
