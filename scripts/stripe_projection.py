@@ -4,7 +4,7 @@ Every stripe of a G-way split (bench.py's equal-area row stripes) is run on
 its own, timed with CUDA events, and the cross-stripe stitch is timed on the
 gathered summaries.  The projection for G GPUs is the slowest stripe plus the
 stitch plus the NCCL exchange at NVLink rate (summaries 16 B/column/rank
-all-gathered, 24 MiB histograms reduced); it ignores everything the one-GPU
+gathered to rank 0, 24 MiB histograms reduced); it ignores everything the one-GPU
 measurement cannot see (NCCL latency, clock differences between GPUs).
 """
 import json
