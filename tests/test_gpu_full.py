@@ -76,7 +76,7 @@ def test_full_size_bit_exact(tag):
                 assert m[k] == pytest.approx(v, rel=1e-12, abs=0), k
 
 
-@pytest.mark.parametrize("tag", [t for t in FULL if t in ("C3", "P")])
+@pytest.mark.parametrize("tag", [t for t in FULL if t in ("C3", "P", "C5")])
 def test_full_size_multi_stripe(tag):
     """Three stripes on one GPU (rqa_run_multi: device-side reduction + stitch)."""
     fx, s = _load(tag)
