@@ -42,19 +42,41 @@ struct SymFoldArgs {
 constexpr int kFoldBatch = 8;
 
 // Block-local line histogram of the fold kernels: shared 32-bit bins for
-// lengths < kSmemBins (runs that cross segment edges are plentiful, e.g. one
-// white run per hook and band), flushed once per block.
+// lengths < kFoldBins (runs that cross segment edges are plentiful, e.g. one
+// white run per hook and band), flushed once per block; longer runs go to
+// 64-bit global atomics.  Wider than the band kernel's bins: junction runs of
+// smooth data are often longer than a band, and global atomics on a few hot
+// lengths serialise in L2.
+#ifndef RQA_FOLD_BINS
+#define RQA_FOLD_BINS 4096
+#endif
+constexpr int kFoldBins = RQA_FOLD_BINS;
+
+struct FoldHist {
+  uint32_t sh;               // shared-window address of [3][kFoldBins] u32 bins
+  unsigned long long* g;     // [3][n+1]
+  int64_t stride;            // n+1
+  __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
+    if (len < kFoldBins) {
+      const uint32_t addr = sh + 4u * (uint32_t)(kind * kFoldBins + (int)len);
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
+    } else {
+      atomicAdd(&g[kind * stride + len], (unsigned long long)w);
+    }
+  }
+};
+
 struct FoldBins {
   uint32_t* sh;
   __device__ __forceinline__ void init() {
-    for (int q = threadIdx.x; q < 3 * kSmemBins; q += blockDim.x) sh[q] = 0u;
+    for (int q = threadIdx.x; q < 3 * kFoldBins; q += blockDim.x) sh[q] = 0u;
     __syncthreads();
   }
   __device__ __forceinline__ void flush(unsigned long long* g, int64_t n) {
     __syncthreads();
-    for (int q = threadIdx.x; q < 3 * kSmemBins; q += blockDim.x) {
+    for (int q = threadIdx.x; q < 3 * kFoldBins; q += blockDim.x) {
       const uint32_t c = sh[q];
-      if (c) atomicAdd(&g[(q / kSmemBins) * (n + 1) + (q % kSmemBins)], (unsigned long long)c);
+      if (c) atomicAdd(&g[(q / kFoldBins) * (n + 1) + (q % kFoldBins)], (unsigned long long)c);
     }
   }
 };
@@ -74,7 +96,7 @@ __device__ __forceinline__ void fold_diag_body(const SymFoldArgs& a, const int m
   const int64_t n = a.n;
   FoldBins fb{bins};
   fb.init();
-  const Hist h{smem_u32(bins), a.hist, n + 1};
+  const FoldHist h{smem_u32(bins), a.hist, n + 1};
   // a thread folds diagonals t and n-1-t: their segment counts add up to
   // about the same for every thread (the upper triangle is balanced)
   for (int64_t t = bid * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
@@ -140,7 +162,7 @@ __device__ __forceinline__ void fold_diag_body(const SymFoldArgs& a, const int m
 }
 
 __global__ void __launch_bounds__(256, 4) sym_fold_diag(const SymFoldArgs a, const int mode) {
-  __shared__ uint32_t bins[3 * kSmemBins];
+  __shared__ uint32_t bins[3 * kFoldBins];
   fold_diag_body(a, mode, blockIdx.x, gridDim.x, bins);
 }
 
@@ -171,7 +193,7 @@ __device__ __forceinline__ void fold_hooks_body(const UnitFoldArgs& a, const int
   const int64_t n = a.n;
   FoldBins fb{bins};
   fb.init();
-  const Hist h{smem_u32(bins), a.hist, n + 1};
+  const FoldHist h{smem_u32(bins), a.hist, n + 1};
   // a thread folds hooks t and n-1-t (balanced band counts, as sym_fold_diag)
   for (int64_t t = bid * (int64_t)blockDim.x + threadIdx.x; t < (n + 1) / 2;
        t += nblk * blockDim.x)
@@ -247,7 +269,7 @@ __device__ __forceinline__ void fold_hooks_body(const UnitFoldArgs& a, const int
 }
 
 __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, const int mode) {
-  __shared__ uint32_t bins[3 * kSmemBins];
+  __shared__ uint32_t bins[3 * kFoldBins];
   fold_hooks_body(a, mode, blockIdx.x, gridDim.x, bins);
 }
 
@@ -255,7 +277,7 @@ __global__ void __launch_bounds__(256, 4) unit_fold_hooks(const UnitFoldArgs a, 
 // fold hooks (independent inputs; the two latency-bound folds overlap).
 __global__ void __launch_bounds__(256, 4) unit_fold_all(const SymFoldArgs d, const UnitFoldArgs u,
                                                         const int mode, const int diag_blocks) {
-  __shared__ uint32_t bins[3 * kSmemBins];
+  __shared__ uint32_t bins[3 * kFoldBins];
   if ((int)blockIdx.x < diag_blocks)
     fold_diag_body(d, mode, blockIdx.x, diag_blocks, bins);
   else

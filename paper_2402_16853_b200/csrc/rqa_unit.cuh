@@ -993,6 +993,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       }
     }
     if (((it + 1) & 4095) == 0) {
+      // 32-bit shared bins are emptied into the 64-bit histogram every 4096
+      // iterations (no overflow); first every warp's adds of this iteration
+      // (the diagonal pieces closed above) must have landed
+      __syncthreads();
       for (int q = tid; q < 3 * kSmemBins; q += NW * 32) {
         const uint32_t cnt = sh_hist[q];
         if (cnt) {

@@ -18,6 +18,8 @@ import pytest
 
 from fixtures import GOLDEN, assert_same, result_arrays
 
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 pytestmark = pytest.mark.gpu
 
 
@@ -86,3 +88,40 @@ def test_full_size_multi_stripe(tag):
     got = (h.diagonal, h.vertical, h.white_vertical, h.recurrence_points)
     assert_same(got, result_arrays(fx["result"]), f"full {tag} x3")
     assert timing["bands"] == 3
+
+
+_CHILD_LONG_UNITS = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+from paper_2402_16853_b200 import embed, run_analysis
+from paper_2402_16853_b200.workloads import WORKLOADS
+wl = WORKLOADS["C3"]
+st = wl.settings
+e = embed(wl.series(), st.embedding_dimension, st.time_delay)
+out = []
+for _ in range(3):
+    h, t = run_analysis(e, st, device=0)
+    out.append([int(h.recurrence_points), {str(k): int(v) for k, v in enumerate(h.diagonal) if v},
+                {str(k): int(v) for k, v in enumerate(h.vertical) if v},
+                {str(k): int(v) for k, v in enumerate(h.white_vertical) if v}])
+print(json.dumps(out))
+"""
+
+
+def test_long_work_units_in_subprocess():
+    """RQA_WAVES=1: one wave of units, each > 4096 iterations, so every unit
+    empties its 32-bit shared bins into the 64-bit histogram mid-run (the
+    path C5 takes by default; a missing barrier there lost a few diagonal
+    runs nondeterministically).  Three runs of full C3 must equal the golden."""
+    import subprocess
+    import sys
+
+    fx, _ = _load("C3")
+    env = dict(os.environ, RQA_WAVES="1")
+    out = subprocess.run([sys.executable, "-c", _CHILD_LONG_UNITS, REPO], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    want = fx["result"]
+    for pts, d, v, w in json.loads(out.stdout.strip().splitlines()[-1]):
+        assert pts == want["recurrence_points"]
+        assert d == want["diagonal"] and v == want["vertical"] and w == want["white_vertical"]
