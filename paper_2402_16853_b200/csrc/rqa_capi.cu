@@ -646,6 +646,9 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.points = points;
   static const char* skip_env = getenv("RQA_SKIP");  // profiling only: skip phases
   a.skip = skip_env ? atoi(skip_env) : 0;
+  static const char* flush_env = getenv("RQA_FLUSH_EVERY");  // tests: power of two
+  const int flush_every = flush_env ? std::max(1, atoi(flush_env)) : 4096;
+  a.flush_mask = ((flush_every & (flush_every - 1)) == 0 ? flush_every : 4096) - 1;
   a.timers = nullptr;
   a.sf = p.sf;
   a.c32 = p.c32;

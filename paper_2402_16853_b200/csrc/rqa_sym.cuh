@@ -35,6 +35,8 @@ struct SymArgs {
   unsigned long long* hist;  // [3][n+1]
   unsigned long long* points;
   int skip;                  // profiling only (RQA_SKIP): 1 diag runs, 2 row phase, 4 column phase
+  int flush_mask;            // shared bins emptied when ((iteration + 1) & flush_mask) == 0
+                             // (4095; RQA_FLUSH_EVERY=2^k for tests of that path)
   unsigned long long* timers;  // profiling only (RQA_TIMERS): [4] cycles compute/rows/cols/other
   // f32 filter kernels (PREC = 1, rqa_unit.cuh): float32 evaluation with a
   // certified band around the threshold; words with a cell inside the band

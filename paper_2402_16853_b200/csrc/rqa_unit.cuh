@@ -992,7 +992,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         }
       }
     }
-    if (((it + 1) & 4095) == 0) {
+    if (((it + 1) & a.flush_mask) == 0) {
       // 32-bit shared bins are emptied into the 64-bit histogram every 4096
       // iterations (no overflow); first every warp's adds of this iteration
       // (the diagonal pieces closed above) must have landed

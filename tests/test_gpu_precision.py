@@ -266,3 +266,38 @@ def test_fp32_mode_measures_relative_error(tag, length):
         assert e <= bound, (tag, k, e, rep["mismatched_cells"])
     for k in ("L_max", "V_max", "W_max"):
         assert rep["measures_fp32"][k] == rep["measures_fp64"][k], k
+
+
+_CHILD_FLUSH = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2402_16853_b200 import AnalysisSettings, embed, run_analysis
+from oracle.oracle import oracle_histograms
+out = []
+rng = np.random.default_rng(5)
+for kind, m, tau, metric, r, w in (("uniform", 3, 1, "l2", 0.15, 0), ("sine", 2, 2, "l2", 0.5, 1),
+                                   ("sine", 10, 5, "l1", 3.0, 10), ("uniform", 3, 2, "linf", 0.1, 0)):
+    n = 9000
+    s = rng.uniform(0, 1, n) if kind == "uniform" else np.sin(np.linspace(0, 90, n)) + 0.1 * rng.normal(size=n)
+    st = AnalysisSettings(m, tau, metric, r, theiler_corrector=w)
+    for devices in ([0], [0, 0]):
+        h, t = run_analysis(embed(s, m, tau), st, devices=devices)
+        d, v, wh, p = oracle_histograms(s, m, tau, metric, r, w, tile_size=512)
+        ok = (h.recurrence_points == p and (h.diagonal == d).all() and (h.vertical == v).all()
+              and (h.white_vertical == wh).all())
+        out.append([kind, m, metric, len(devices), bool(ok)])
+print(json.dumps(out))
+"""
+
+
+def test_shared_bin_flush_every_two_iterations_in_subprocess():
+    """RQA_FLUSH_EVERY=2: the band kernel empties its 32-bit shared bins into
+    the 64-bit histogram every second iteration (by default every 4096, which
+    only units of C5-size runs reach); every result must stay exact."""
+    env = dict(os.environ, RQA_FLUSH_EVERY="2", RQA_PREFILTER="1")
+    out = subprocess.run([sys.executable, "-c", _CHILD_FLUSH, REPO], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    for kind, m, metric, g, ok in json.loads(out.stdout.strip().splitlines()[-1]):
+        assert ok, (kind, m, metric, g)
