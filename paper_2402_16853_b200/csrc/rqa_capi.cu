@@ -536,11 +536,11 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
     X[b] = (nrem + D - 1) / D + R - 1;
     total += X[b];
   }
-  // aim for >= 16 waves of units (RQA_WAVES overrides; 4 waves left a 5-8 %
-  // tail, measured with scripts/stripe_projection.py); one recomputed
-  // iteration per unit boundary
+  // aim for >= 32 waves of units (RQA_WAVES overrides; 4 waves left a 5-8 %
+  // tail in round 1; round-2 sweep 8..96: 32 best for C3 / P, C4 flat); one
+  // recomputed iteration per unit boundary
   static const char* wenv = getenv("RQA_WAVES");
-  const int64_t waves = wenv ? std::max(1, atoi(wenv)) : 16;
+  const int64_t waves = wenv ? std::max(1, atoi(wenv)) : 32;
   // units of >= 16 iterations keep the recomputed iteration <= 1/16 of the
   // work, unless the whole triangle is too small to fill the GPU once (C1):
   // then parallelism wins over the recomputation
