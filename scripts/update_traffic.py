@@ -33,7 +33,7 @@ folds = collections.defaultdict(list)
 for r in csv.DictReader(line for line in open(launches) if not line.startswith("==")):
     if r.get("Metric Name") == "gpu__time_duration.sum":
         name = r["Kernel Name"]
-        for f in ("sym_fold_diag", "unit_fold_hooks", "fix_diag_pieces"):
+        for f in ("sym_fold_diag", "unit_fold_hooks", "unit_fold_all", "fix_diag_pieces"):
             if f in name:
                 v = float(r["Metric Value"].replace(",", ""))
                 folds[f].append(v * (1e-6 if r["Metric Unit"] == "ns" else
