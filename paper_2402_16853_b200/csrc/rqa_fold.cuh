@@ -352,9 +352,14 @@ struct UnitStitchArgs {
   unsigned long long* hist;
 };
 
-__global__ void unit_fold_stripes(const UnitStitchArgs a) {
+__global__ void __launch_bounds__(256, 4) unit_fold_stripes(const UnitStitchArgs a) {
   const int64_t n = a.n;
-  const GHist h{a.hist, n + 1};
+  // block-local bins as in the folds (global atomics on a few hot lengths
+  // serialise in L2)
+  __shared__ uint32_t bins[3 * kFoldBins];
+  FoldBins fb{bins};
+  fb.init();
+  const FoldHist h{smem_u32(bins), a.hist, n + 1};
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     {
@@ -372,10 +377,10 @@ __global__ void unit_fold_stripes(const UnitStitchArgs a) {
           continue;
         }
         const int64_t x = open + p;
-        if (x > 0) atomicAdd(&a.hist[kDiag * (n + 1) + x], wgt);
+        if (x > 0) h.add(kDiag, x, (uint32_t)wgt);
         open = (hi <= rows) ? (int64_t)a.ss[g * n + k] : 0;
       }
-      if (open > 0) atomicAdd(&a.hist[kDiag * (n + 1) + open], wgt);
+      if (open > 0) h.add(kDiag, open, (uint32_t)wgt);
     }
     {
       const int64_t c = k;
@@ -393,6 +398,7 @@ __global__ void unit_fold_stripes(const UnitStitchArgs a) {
       seg_flush(seg_combine(acc, row, h), h);
     }
   }
+  fb.flush(a.hist, n);
 }
 
 }  // namespace rqa
