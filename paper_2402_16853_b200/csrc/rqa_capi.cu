@@ -536,11 +536,16 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
     X[b] = (nrem + D - 1) / D + R - 1;
     total += X[b];
   }
-  // aim for >= 32 waves of units (RQA_WAVES overrides; 4 waves left a 5-8 %
-  // tail in round 1; round-2 sweep 8..96: 32 best for C3 / P, C4 flat); one
-  // recomputed iteration per unit boundary
+  // waves of units: more waves shorten the tail of the launch, fewer waves
+  // recompute fewer boundary iterations (one per unit).  Measured optimum
+  // (round 2): 32 waves for a whole 2^20 run (~7,100 iterations per resident
+  // CTA), 16 for one of 8 stripes of it (~890): waves = 16 (T / 887)^(1/3),
+  // T = iterations per resident CTA, clamped to [8, 64]; RQA_WAVES overrides
   static const char* wenv = getenv("RQA_WAVES");
-  const int64_t waves = wenv ? std::max(1, atoi(wenv)) : 32;
+  const double per_slot = (double)total / std::max(1, slots);
+  const int64_t waves = wenv ? std::max(1, atoi(wenv))
+                             : std::min<int64_t>(64, std::max<int64_t>(
+                                   8, std::llround(16.0 * std::cbrt(per_slot / 887.0))));
   // units of >= 16 iterations keep the recomputed iteration <= 1/16 of the
   // work, unless the whole triangle is too small to fill the GPU once (C1):
   // then parallelism wins over the recomputation
