@@ -13,12 +13,23 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rqa_b200.h"
 #include "rqa_fold.cuh"
 #include "rqa_variants.cuh"
 
 namespace rqa {
 namespace {
+
+// NVTX range over a host-side phase (header-only NVTX 3: free without a
+// profiler attached; nsys / ncu --nvtx show the phases of every call).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 std::atomic<int64_t> g_launches{0};
 
@@ -354,6 +365,7 @@ int cuda_fail(cudaError_t e, const char* what, char* err, size_t errlen) {
 // Stage the series into the zero-padded workspace buffer.
 int stage_series(Workspace* ws, const Problem& p, const double* src, cudaMemcpyKind kind,
                  cudaStream_t st, char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa.stage_series");
   const size_t need = (size_t)(p.len + 2 * p.pad);
   RQA_CUDA(grow(&ws->s_pad, &ws->s_cap, need), "allocating series buffer");
   RQA_CUDA(cudaMemsetAsync(ws->s_pad, 0, (size_t)p.pad * sizeof(double), st), "memset pad");
@@ -461,6 +473,7 @@ int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t
 inline double prefilter_max(int m) { return 0.05 * std::max(1.0, m / 3.0); }
 
 int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa.plan_prefilter");
   if (p->precision != 64 || p->filt != -1) return RQA_OK;
   static const char* penv = getenv("RQA_PREFILTER");
   const int want = penv ? atoi(penv) : 2;
@@ -606,6 +619,7 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
                 unsigned long long* hist, unsigned long long* points, int32_t* out_p,
                 int32_t* out_s, uint32_t* out_col, uint32_t* out_row, cudaStream_t st,
                 cudaEvent_t ev_mid, char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa.launch_rows");
   const int64_t H = p.var.band_rows(), HS = p.var.slot_rows();
   const int64_t nb = (row_hi - row_lo + H - 1) / H;
   if (nb <= 0) return RQA_OK;
@@ -757,6 +771,7 @@ int stitch_stripes(Workspace* ws, const int32_t* d_prefix, const int32_t* d_suff
                    const uint32_t* d_col, const uint32_t* d_row, const int64_t* bounds,
                    int32_t nstripes, int64_t n, unsigned long long* hist, cudaStream_t st,
                    char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa.stitch");
   RQA_CUDA(grow(&ws->bounds, &ws->bounds_cap, (size_t)nstripes + 1), "allocating bounds");
   RQA_CUDA(cudaMemcpyAsync(ws->bounds, bounds, (nstripes + 1) * sizeof(int64_t),
                            cudaMemcpyHostToDevice, st),
@@ -831,6 +846,7 @@ int run_full(Workspace* ws, const Problem& p, unsigned long long* hist, unsigned
 int copy_out(Workspace* ws, const unsigned long long* hist, size_t hn, int32_t flags, int64_t* diag,
              int64_t* vert, int64_t* white, int64_t* points, int64_t* mismatches, cudaStream_t st,
              char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa.copy_out");
   // outputs: the nonzero bins only when the caller's arrays are zero-filled
   // (RQA_FLAG_OUT_ZEROED) and they fit the pair buffer, else dense copies
   bool dense = true;
@@ -914,6 +930,7 @@ struct StripeJob {
 };
 
 int run_stripe_job(StripeJob* j, const Problem& p0, const double* series) {
+  NvtxRange nvtx_("rqa.stripe_job");
   char* err = j->err;
   const size_t errlen = sizeof j->err;
   RQA_CUDA(cudaSetDevice(j->dev), "cudaSetDevice");
@@ -997,6 +1014,7 @@ int rqa_run_prec(const double* series, int64_t len, int32_t m, int32_t tau, int3
                  double radius, int64_t theiler, int32_t precision, int32_t device,
                  int32_t flags, int64_t* diag, int64_t* vert, int64_t* white, int64_t* points,
                  int64_t* mismatches, double* timing, char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa_run_prec");
   if (!series || !diag || !vert || !white || !points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
   if (precision != 64 && precision != 32)
@@ -1062,6 +1080,7 @@ int rqa_run_multi(const double* series, int64_t len, int32_t m, int32_t tau, int
                   int32_t n_devices, int32_t flags, int64_t* diag, int64_t* vert, int64_t* white,
                   int64_t* points, int64_t* mismatches, double* timing, char* err,
                   size_t errlen) {
+  NvtxRange nvtx_("rqa_run_multi");
   if (!series || !diag || !vert || !white || !points || !devices)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
   if (precision != 64 && precision != 32)
@@ -1200,6 +1219,7 @@ int rqa_run_device_prec(const double* d_series, int64_t len, int32_t m, int32_t 
                         int64_t* d_points, int64_t* d_mismatches, int32_t* d_stripe_prefix,
                         int32_t* d_stripe_suffix, uint32_t* d_stripe_col, uint32_t* d_rowlead,
                         void* stream, char* err, size_t errlen) {
+  NvtxRange nvtx_("rqa_run_device");
   if (!d_series || !d_hist || !d_points)
     return set_err(err, errlen, "null pointer argument"), RQA_EINVAL;
   if (precision != 64 && precision != 32)
