@@ -78,6 +78,17 @@ int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t *ba
                   int32_t *reuse_kernel);
 
 /*
+ * Host-only diagnostic: the work-unit plan of the band kernel for n vectors,
+ * rows [row_lo, row_hi), bands of band_rows = r * slot_rows rows and `slots`
+ * resident CTAs (no device needed).  Writes up to cap units as (band, xa, xb)
+ * triples in band order (iteration ranges of each band's diagonal sweep) and
+ * *count (the full number, also when > cap).  The plan replaces the
+ * reference's tile partition (engine.py:86-126) as the unit of scheduling.
+ */
+int rqa_plan_units(int64_t n, int64_t row_lo, int64_t row_hi, int32_t slot_rows, int32_t r,
+                   int32_t slots, int32_t *units, int64_t cap, int64_t *count);
+
+/*
  * Full analysis of a host series on one device: replaces run_analysis
  * (engine.py:215-280).  Writes the three histograms (int64[n+1] each, n =
  * len - (m-1)*tau), the recurrence point count and RQA_TIMING_SLOTS timings.

@@ -30,6 +30,7 @@ SYMBOLS = {
     "rqa_launch_counter": (_i64, []),
     "rqa_threshold": (_c.c_int, [_i32, _i32, _dbl, _pd]),
     "rqa_band_rows": (_c.c_int, [_i32, _i32, _i32, _i64, _pi64, _pi32]),
+    "rqa_plan_units": (_c.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _pi32, _i64, _pi64]),
     "rqa_run": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _pi64, _pi64,
                            _pi64, _pi64, _pd, _c.c_char_p, _c.c_size_t]),
     "rqa_run_prec": (_c.c_int, [_pd, _i64, _i32, _i32, _i32, _dbl, _i64, _i32, _i32, _i32,

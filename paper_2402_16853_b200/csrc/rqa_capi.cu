@@ -999,6 +999,26 @@ int rqa_threshold(int32_t metric, int32_t m, double radius, double* thr) {
   return RQA_OK;
 }
 
+int rqa_plan_units(int64_t n, int64_t row_lo, int64_t row_hi, int32_t slot_rows, int32_t r,
+                   int32_t slots, int32_t* units, int64_t cap, int64_t* count) {
+  if (!count || n < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi || slot_rows < 32 ||
+      slot_rows % 32 != 0 || r < 1 || slots < 1 || (cap > 0 && !units))
+    return RQA_EINVAL;
+  Problem p;
+  memset(&p.var, 0, sizeof p.var);
+  p.n = n;
+  p.var.nw = slot_rows / 32;
+  p.var.r = r;
+  const UnitPlan pl = plan_units(p, row_lo, row_hi, slots);
+  *count = (int64_t)pl.by_band.size();
+  for (int64_t q = 0; q < std::min<int64_t>(cap, *count); ++q) {
+    units[3 * q] = pl.by_band[q].x;
+    units[3 * q + 1] = pl.by_band[q].y;
+    units[3 * q + 2] = pl.by_band[q].z;
+  }
+  return RQA_OK;
+}
+
 int rqa_band_rows(int32_t metric, int32_t m, int32_t tau, int64_t n, int64_t* band_rows,
                   int32_t* reuse_kernel) {
   Variant v;
