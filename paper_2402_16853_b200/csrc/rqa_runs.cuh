@@ -119,7 +119,10 @@ __device__ __forceinline__ void runs_consume(uint32_t x, int nb, RunState& st, c
 constexpr int kQueueCap = 128;  // events per warp (16 bytes each)
 // Drain when this many events are queued: every check follows at most 64
 // pushes (two 64-bit words per lane), so the ring never holds more than 127.
-constexpr uint32_t kDrainAt = 64u;
+#ifndef RQA_DRAIN_AT
+#define RQA_DRAIN_AT 64u
+#endif
+constexpr uint32_t kDrainAt = RQA_DRAIN_AT;
 
 // Event (16 bytes): x, y = boundary mask (bits 0..31, 32..63), z = carried
 // run (len << 1 | bit) in bits 0..28 plus flags in bits 29..31: bit 29 skip

@@ -110,7 +110,10 @@ __device__ __forceinline__ uint2 f32_recheck(const SymArgs& a, int64_t row0, int
 // entries); long sums (m >= 5) list cells, appended per slot word, 512
 // entries (two CTAs per SM still fit).
 template <int PREC, int M>
-constexpr int kCandCapOf = (PREC != 2) ? 0 : (M <= 4 ? 256 : 512);
+#ifndef RQA_CAND_CAP_LONG
+#define RQA_CAND_CAP_LONG 512
+#endif
+constexpr int kCandCapOf = (PREC != 2) ? 0 : (M <= 4 ? 256 : RQA_CAND_CAP_LONG);
 // Short-window prefilter kernels evaluate the per-component predicate in
 // packed float32 (sub/fma.rn.f32x2 over slot pairs, the sign bit of
 // d32*d32 - D32^2 funnel-shifted into the word): 2.5 instructions per cell
