@@ -1,5 +1,9 @@
 """Contract tests on the GPU: the documented drop-in binding and SPEC.md's
-acceptance criterion 3 (metric monotonicity)."""
+acceptance criteria 3 (metric monotonicity) and 4 (reduced-scale paper
+benchmark, invariant across workers and devices).  Criterion 5 (NOAA
+Asheville data) is waived: the data is not available offline (SPEC.md:469
+allows the waiver); criteria 1, 2, 6 and 7 are tests/test_oracle_golden.py,
+test_gpu_parity.py, test_gpu_plot.py and test_ingest_native.py."""
 
 import os
 import re
@@ -114,3 +118,38 @@ def test_metric_monotonicity():
         assert rr["linf"] >= rr["l2"] >= rr["l1"], (i, m, tau, eps, rr)
         cases += 1
     assert cases >= 50
+
+
+def test_spec_criterion_4_reduced_paper_benchmark(tmp_path, oracle_lib):
+    """SPEC.md:468 (acceptance criterion 4): n = 100,001 points of the paper's
+    sine with x_end = 100 pi, m = 2, tau = 2, eps = 1.0, all minimums 2,
+    through the CLI.  The JSON measures and histograms must be identical for
+    every worker count and device list (the reference's parallel-correctness
+    notion), bit-exact against the C oracle, and the run
+    fast (the scaling requirement, restated for one B200: well under 1 s of
+    device time for the 10^10-cell matrix)."""
+    import json
+
+    from paper_2402_16853_b200.cli import main
+    from paper_2402_16853_b200.ingest import generate_sine
+
+    outs = []
+    for extra in (["--workers", "1"], ["--workers", "4"], ["--devices", "0,0,0,0"]):
+        path = tmp_path / f"out{len(outs)}.json"
+        argv = ["rqa", "--synthetic-sine", "100001", "--x-end-pi-multiples", "100",
+                "--embedding", "2", "--delay", "2", "--metric", "euclidean", "--radius", "1.0",
+                "--output", str(path)] + extra
+        assert main(argv) == 0
+        outs.append(json.loads(path.read_text()))
+    for o in outs[1:]:
+        assert o["measures"] == outs[0]["measures"]
+        assert o["histograms"] == outs[0]["histograms"]
+        assert o["recurrence_points"] == outs[0]["recurrence_points"]
+    assert outs[0]["timing"]["device_total"] < 1.0
+    s = np.asarray(generate_sine(100001, 100 * np.pi).values, np.float64)
+    d, v, w, p = oracle_lib.oracle_histograms(s, 2, 2, "l2", 1.0, 0, tile_size=1024)
+    assert outs[0]["recurrence_points"] == p
+    for kind, ref in (("diagonal", d), ("vertical", v), ("white_vertical", w)):
+        got = {int(k): c for k, c in outs[0]["histograms"][kind].items()}
+        want = {int(k): int(c) for k, c in enumerate(ref) if c}
+        assert got == want, kind
