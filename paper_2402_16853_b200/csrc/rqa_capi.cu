@@ -144,19 +144,22 @@ struct Workspace {
   int64_t plan_nunits = 0;
 };
 
-// Resident CTAs per SM of a kernel variant (queried once per kernel).
+// Resident CTAs per SM of a kernel variant (queried once per kernel and device).
 int variant_occupancy(const Variant& v, int* per_sm) {
   static std::mutex mu;
-  static std::vector<std::pair<const void*, int>> cache;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<const void*, int> key(v.kernel, dev);
   std::lock_guard<std::mutex> lk(mu);
   for (const auto& e : cache)
-    if (e.first == v.kernel) return *per_sm = e.second, 0;
+    if (e.first == key) return *per_sm = e.second, 0;
   cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)v.smem);
   if (e == cudaSuccess)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, v.kernel, 32 * v.nw, v.smem);
   if (e != cudaSuccess) return (int)e;
-  cache.emplace_back(v.kernel, *per_sm);
+  cache.emplace_back(key, *per_sm);
   return 0;
 }
 
