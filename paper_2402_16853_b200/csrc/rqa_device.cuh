@@ -15,7 +15,10 @@ enum Metric : int { kL1 = 0, kL2 = 1, kLinf = 2 };
 enum HistKind : int { kDiag = 0, kVert = 1, kWhite = 2 };
 
 // Shared-memory histogram bins per kind; longer lines go to global memory.
-constexpr int kSmemBins = 1024;
+#ifndef RQA_SMEM_BINS
+#define RQA_SMEM_BINS 1024
+#endif
+constexpr int kSmemBins = RQA_SMEM_BINS;
 
 // Per-lane constants of the rotate-and-select 32x32 bit transpose: stage j
 // exchanges j-blocks with lane^j; the partner word is rotated left by j (or
