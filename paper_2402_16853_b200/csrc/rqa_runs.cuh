@@ -159,14 +159,22 @@ __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
   uint32_t p = (uint32_t)__ffsll((long long)bnd) - 1u;
   uint32_t len = (ecur >> 1) + p;
   uint32_t wt = (flags & 1u) ? 0u : (bit ? w1 : w0);
+  bnd &= bnd - 1ull;
+  // two runs per trip: the second run's boundary scan does not wait for the
+  // first run's histogram add (more independent work per lane)
   for (;;) {
     hist_red(h, bit ? k1 : k0, len, wt);  // wt == 0: predicated off
-    bnd &= bnd - 1ull;
     if (bnd == 0ull) break;
-    const uint32_t q = (uint32_t)__ffsll((long long)bnd) - 1u;
-    len = q - p;
-    p = q;
-    bit ^= 1u;
+    const uint32_t q1 = (uint32_t)__ffsll((long long)bnd) - 1u;
+    const unsigned long long b2 = bnd & (bnd - 1ull);
+    const uint32_t bit1 = bit ^ 1u;
+    hist_red(h, bit1 ? k1 : k0, q1 - p, bit1 ? w1 : w0);
+    if (b2 == 0ull) break;
+    const uint32_t q2 = (uint32_t)__ffsll((long long)b2) - 1u;
+    len = q2 - q1;
+    p = q2;
+    bnd = b2 & (b2 - 1ull);
+    bit = bit1 ^ 1u;
     wt = bit ? w1 : w0;
   }
 }
