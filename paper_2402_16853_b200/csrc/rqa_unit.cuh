@@ -780,14 +780,19 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     // ---- row phase (not in the recomputed iteration): row parts of hooks
     const uint32_t* prev_cur = prevbuf + buf * H;    // words of iteration x-1, warp NW-1
     uint32_t* prev_next = prevbuf + (buf ^ 1) * H;
-    constexpr int PR = (R % 2 == 0) ? 2 : 1;
+    constexpr int PR = (R % 2 == 0) ? 2 : 1;  // slot pairs (column phase)
+    // rows per thread handled together in the row phase (independent run
+    // states interleave; a drain check after every two passes): all R slots
+    // for the prefilter kernels (sparse by construction: C3 -0.45 %), pairs
+    // otherwise (dense data, P: 4 measured +2 %)
+    constexpr int PRR = (PREC == 2 && R % 4 == 0) ? 4 : PR;
 #pragma unroll 1
-    for (int r0 = 0; r0 < R; r0 += PR) {
-      int lr[PR], rem[PR];
-      RunState rs[PR];
+    for (int r0 = 0; r0 < R; r0 += PRR) {
+      int lr[PRR], rem[PRR];
+      RunState rs[PRR];
       bool any_rem = false, all_full = true;
 #pragma unroll
-      for (int p = 0; p < PR; ++p) {
+      for (int p = 0; p < PRR; ++p) {
         const int r = r0 + p;
         lr[p] = r * HS + tid;
         prev_next[lr[p]] = rowbuf[(NW - 1) * H + lr[p]];
@@ -798,38 +803,38 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       }
       if (!(skip & 2) && __any_sync(0xffffffffu, any_rem)) {
 #pragma unroll
-        for (int p = 0; p < PR; ++p) {
+        for (int p = 0; p < PRR; ++p) {
           const uint2 rsv = rowst[lr[p]];
           rs[p] = RunState{rsv.x, rsv.y};
         }
         if (__all_sync(0xffffffffu, all_full)) {
-          static_assert(NW % 2 == 0 && PR <= 2, "row phase: PR pushes of 64 bits per drain check");
+          static_assert(NW % 2 == 0, "row phase: word pairs");
 #pragma unroll 1
           for (int v = 0; v < NW; v += 2) {
 #pragma unroll
-            for (int p = 0; p < PR; ++p) {
+            for (int p = 0; p < PRR; ++p) {
               const uint32_t w0 = rowbuf[v * H + lr[p]], w1 = rowbuf[(v + 1) * H + lr[p]];
               pts += __popc(w0) + __popc(w1);
               runs_push(w0, w1, 64, rs[p], 0u, evq);
+              if (p % 2 == 1 || p == PRR - 1) queue_check(evq, hist, lane);
             }
-            queue_check(evq, hist, lane);
           }
         } else {
 #pragma unroll 1
           for (int v = 0; v < NW; v += 2) {
 #pragma unroll
-            for (int p = 0; p < PR; ++p) {
+            for (int p = 0; p < PRR; ++p) {
               const int nb = min(max(rem[p] - 32 * v, 0), 64);
               const uint32_t w0 = rowbuf[v * H + lr[p]] & low_mask(nb);
               const uint32_t w1 = rowbuf[(v + 1) * H + lr[p]] & (nb > 32 ? low_mask(nb - 32) : 0u);
               pts += __popc(w0) + __popc(w1);
               runs_push(w0, w1, nb, rs[p], 0u, evq);
+              if (p % 2 == 1 || p == PRR - 1) queue_check(evq, hist, lane);
             }
-            queue_check(evq, hist, lane);
           }
         }
 #pragma unroll
-        for (int p = 0; p < PR; ++p) {
+        for (int p = 0; p < PRR; ++p) {
           const int r = r0 + p;
           if (rem[p] > 0 && x == r) pts64 -= (rowbuf[lr[p]] & 1u);  // diagonal cell once
           rowst[lr[p]] = make_uint2(rs[p].first, rs[p].cur);
