@@ -853,11 +853,16 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       const int cfin = kx + 32 * wv + lane;
       const int cnew = cfin + D;
 #pragma unroll 1
-      for (int rr0 = 0; rr0 < R; rr0 += PR) {
-        int rs_[PR], lim_fin[PR], lim_new[PR];
-        RunState cur[PR], nst[PR], fin[PR];
+#ifndef RQA_COL_PR
+#define RQA_COL_PR 2
+#endif
+      // slots handled together in the column phase
+      constexpr int PC = (R % RQA_COL_PR == 0) ? RQA_COL_PR : PR;
+      for (int rr0 = 0; rr0 < R; rr0 += PC) {
+        int rs_[PC], lim_fin[PC], lim_new[PC];
+        RunState cur[PC], nst[PC], fin[PC];
 #pragma unroll
-        for (int p = 0; p < PR; ++p) {
+        for (int p = 0; p < PC; ++p) {
           const int r = R - 1 - (rr0 + p);
           rs_[p] = r;
           const uint2 cs = colst[(wv * R + r) * 32 + lane];
@@ -867,7 +872,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           lim_fin[p] = (do_fin && x >= r && cfin < nrem) ? min(cfin, hrows) - r * HS : 0;
           lim_new[p] = (do_new && x >= r && cnew < nrem) ? min(cnew, hrows) - r * HS : 0;
         }
-        if (!(skip & 4) && x >= rs_[PR - 1]) {
+        if (!(skip & 4) && x >= rs_[PC - 1]) {
           // column window c of slot rows: words of warps wp-1 and wp funnel-
           // shifted into aligned columns, transposed, bit-reversed (columns
           // are met bottom-up); all lanes take part (transpose)
@@ -883,7 +888,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           // its top ones: after the bit reversal, its high bits)
           auto col_pair = [&](int c, int lo, const int* lim, auto full) {
 #pragma unroll
-            for (int p = 0; p < PR; ++p) {
+            for (int p = 0; p < PC; ++p) {
               const uint32_t a0 = col_word(c, p);
               const uint32_t a1 = c - 1 >= lo ? col_word(c - 1, p) : 0u;
               if constexpr (decltype(full)::value) {  // every lane: 32 rows per window
@@ -897,8 +902,8 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
                                                ((unsigned long long)b1 << n0);
                 runs_push((uint32_t)x64, (uint32_t)(x64 >> 32), n0 + n1, cur[p], 0u, evq);
               }
+              if (p % 2 == 1 || p == PC - 1) queue_check(evq, hist, lane);
             }
-            queue_check(evq, hist, lane);
           };
           // windows c = hi, hi-1, ..., lo (descending), two per pass
           auto col_steps = [&](int hi, int lo, const int* lim, auto full) {
@@ -909,7 +914,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           using kPart = std::integral_constant<bool, false>;
           bool fnew = true, ffin = true;
 #pragma unroll
-          for (int p = 0; p < PR; ++p) {
+          for (int p = 0; p < PC; ++p) {
             fnew &= lim_new[p] >= 32 * NCH;
             ffin &= lim_fin[p] >= 32 * (wv + 1);
           }
@@ -921,7 +926,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
             else col_steps(NCH - 1, wv + 1, lim_new, kPart{});
           }
 #pragma unroll
-          for (int p = 0; p < PR; ++p) {
+          for (int p = 0; p < PC; ++p) {
             nst[p] = cur[p];
             cur[p] = fin[p];
           }
@@ -931,10 +936,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
             else col_steps(wv, 0, lim_fin, kPart{});
           }
 #pragma unroll
-          for (int p = 0; p < PR; ++p) fin[p] = cur[p];
+          for (int p = 0; p < PC; ++p) fin[p] = cur[p];
         }
 #pragma unroll
-        for (int p = 0; p < PR; ++p) {
+        for (int p = 0; p < PC; ++p) {
           acc = seg_combine(acc, runs_finish(fin[p]), hist);
           colst[(wv * R + rs_[p]) * 32 + lane] = make_uint2(nst[p].cur, nst[p].first);
         }
