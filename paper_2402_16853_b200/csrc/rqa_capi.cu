@@ -702,6 +702,10 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   ua.units = ws->units;
   ua.rowpiece = ws->rowpiece;
   ua.drec = ws->drec;
+  ua.cap_ps = ctot;
+  ua.cap_cs = ctot;
+  ua.cap_drec = nunits * std::max<int64_t>(R - 1, 1) * D;
+  ua.cap_piece = nunits * H;
   RQA_CUDA(p.var.launch(ua, (int)nunits, p.var.w, st), "launching band kernel");
   g_launches++;
   if (ev_mid) RQA_CUDA(cudaEventRecord(ev_mid, st), "event");
@@ -722,6 +726,8 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
     dp.D = D;
     dp.R = (int)R;
     dp.hist = hist;
+    dp.cap_ps = ctot;
+    dp.cap_drec = nunits * (R - 1) * D;
     const int64_t recs = nunits * (R - 1) * D;
     fix_diag_pieces<<<(int)std::min<int64_t>((recs + threads - 1) / threads, 148 * 16), threads, 0,
                       st>>>(dp);

@@ -8,6 +8,32 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
+
+// Checked builds (make EXTRA=-DRQA_CHECKS, scripts/gpu_checked.sh): device
+// bounds / capacity assertions on every global write of the band kernel and
+// the diagonal-piece join, the histogram indices, and the event-ring and
+// candidate-list occupancies.  A failed check prints its condition and traps
+// (the C-ABI call then fails).  Compiled out by default.
+#if defined(RQA_CHECKS) && defined(RQA_CHECKS_TRAP_ONLY)
+#define RQA_DCHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+#elif defined(RQA_CHECKS)
+#define RQA_DCHECK(cond)                                                          \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("RQA_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                         \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define RQA_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 namespace rqa {
 
@@ -87,6 +113,7 @@ struct Hist {
       const uint32_t addr = sh + 4u * (uint32_t)(kind * kSmemBins + (int)len);
       asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
     } else {
+      RQA_DCHECK(len >= 0 && len < stride && kind >= 0 && kind < 3);
       atomicAdd(&g[kind * stride + len], (unsigned long long)w);
     }
   }
@@ -97,6 +124,7 @@ struct GHist {
   unsigned long long* g;
   int64_t stride;
   __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
+    RQA_DCHECK(len >= 0 && len < stride && kind >= 0 && kind < 3);
     atomicAdd(&g[kind * stride + len], (unsigned long long)w);
   }
 };

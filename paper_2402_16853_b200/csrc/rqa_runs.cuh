@@ -143,7 +143,10 @@ __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint3
   const bool small = len < (uint32_t)kSmemBins;
   const uint32_t sa = h.sh + 4u * (small ? kind_row * (uint32_t)kSmemBins + len : kDummyBin);
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa), "r"(small ? w : 0u) : "memory");
-  if (!small && w) atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
+  if (!small && w) {
+    RQA_DCHECK((int64_t)len < h.stride && kind_row < 3u);
+    atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
+  }
 }
 
 __device__ __forceinline__ void expand_event(uint4 e, const Hist& h) {
@@ -253,6 +256,7 @@ __device__ __forceinline__ void runs_push(uint32_t lo, uint32_t hi, int nb, RunS
       "r"(blo), "r"(bhi), "r"(cur | (((diag_weight << 1) | (mkfirst ? 1u : 0u)) << kEvCurBits)),
       "r"(ev ? 1u : 0u));  // no memory clobber: the ring is only accessed through asm
   q.tail += __popc(m);
+  RQA_DCHECK(q.tail - q.head <= (uint32_t)kQueueCap);  // ring never overwrites unread events
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {

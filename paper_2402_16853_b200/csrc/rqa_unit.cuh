@@ -37,6 +37,8 @@ struct UnitArgs {
   uint2* rowpiece;         // [nunits][H]: (first, last) run of each row's piece
   uint2* drec;             // [nunits][R-1][D]: diagonal pieces cut at the unit's end
                            // (x: upper half P | S << 16, y: lower half P | S << 16 | closed << 31)
+  // allocated entries (bounds of the checked build, RQA_CHECKS)
+  int64_t cap_ps, cap_cs, cap_drec, cap_piece;
 };
 
 // ---------------------------------------------------------------------------
@@ -140,6 +142,10 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
   // marks the only cells that can be recurrent, and only those are summed.
   constexpr bool kPre = (PREC == 2) && (M >= 2) && (METRIC != kLinf);
   constexpr bool kAnd = kLinfAnd || kPre;
+#ifndef RQA_RANGE_END
+#define RQA_RANGE_END 0  // A/B: 1 = range test of the segment end in every kernel
+#endif
+  constexpr bool kRangeEnd = kPre || kLinfAnd || RQA_RANGE_END;  // diagonal pieces, below
   constexpr bool kSquare = (METRIC == kL2) && (M >= 2);
   constexpr int NCH = HS / 32;  // == NW
   static_assert(kAnd ? kW <= 96 : kW <= 48, "term window too large");
@@ -511,6 +517,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
                   (uint16_t)((r << 8) | (c << 5) | lane);
             ltail += __popc(mk);
           }
+          RQA_DCHECK(ltail - lhead <= (uint32_t)kCandCap);
           __syncwarp();
           while (ltail - lhead >= 32u) {
             resolve_words(lhead, 32u);
@@ -574,6 +581,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
               cl[pos++ & (uint32_t)(kCandCap - 1)] = (uint16_t)((gi << 10) | (lane << 5) | t);
             }
             ltail += tot;
+            RQA_DCHECK(ltail - lhead <= (uint32_t)kCandCap);
             __syncwarp();
             while (ltail - lhead >= 32u) {
               resolve_cells(lhead, 32u);
@@ -852,12 +860,12 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
       Seg acc{0u, 0u, 0u};
       const int cfin = kx + 32 * wv + lane;
       const int cnew = cfin + D;
-#pragma unroll 1
 #ifndef RQA_COL_PR
 #define RQA_COL_PR 2
 #endif
       // slots handled together in the column phase
       constexpr int PC = (R % RQA_COL_PR == 0) ? RQA_COL_PR : PR;
+#pragma unroll 1
       for (int rr0 = 0; rr0 < R; rr0 += PC) {
         int rs_[PC], lim_fin[PC], lim_new[PC];
         RunState cur[PC], nst[PC], fin[PC];
@@ -944,6 +952,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
           colst[(wv * R + rs_[p]) * 32 + lane] = make_uint2(nst[p].cur, nst[p].first);
         }
       }
+      if (do_fin && cfin < nrem) RQA_DCHECK(cfin >= 0 && (Cb - a.colsum) + cfin < ua.cap_cs);
       if (do_fin && cfin < nrem)
         Cb[cfin] = (cfin == 0) ? 0u
                  : acc.uniform ? pack_col(acc.first, acc.first)
@@ -961,18 +970,30 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
         const int kd = kdr[r];
         if (kd >= 0 && kd < nrem) {
           const int brows = min(hrows, nrem - kd);  // rows of kd in this band
-          const int rend = (brows - 1) / HS;       // slot of its last row
-          if (r == rend) {
+          // slot r ends the segment iff its last row lies in slot r.  The
+          // prefilter and L-inf kernels test the range of brows - 1 - r * HS:
+          // with r == (brows-1)/HS ptxas indexes st[] by the quotient and
+          // moves it to local memory (range test: C3 -1.75 %, C5 -0.27 %,
+          // C4 -0.3 %); the float64 term-reuse kernels keep the quotient (P
+          // measured +0.9 % with the range test)
+          const int lrow = brows - 1 - r * HS;
+          const int rend = (brows - 1) / HS;
+          if (kRangeEnd ? (lrow >= 0 && lrow < HS) : r == rend) {
             const uint32_t ps = diag_piece_end(st[r], brows == hrows,
                                                LineSink{&hist, kd == 0 ? 1u : 2u});
             if (x - r >= xa) {  // the whole band segment was walked by this unit
+              RQA_DCHECK((Pb - a.P) + kd < ua.cap_ps);
               Pb[kd] = (uint16_t)(ps & 0xffffu);
               Sb[kd] = (uint16_t)(ps >> 16);
             } else {  // lower part of a segment cut at xa (upper part: unit idx-1)
+              RQA_DCHECK(unit.idx >= 1 && xa - 1 - (x - r) >= 0 && xa - 1 - (x - r) < R - 1 &&
+                         ((int64_t)(unit.idx - 1) * (R - 1) + (xa - 1 - (x - r))) * D + delta <
+                             ua.cap_drec);
               ua.drec[((int64_t)(unit.idx - 1) * (R - 1) + (xa - 1 - (x - r))) * D + delta].y =
                   ps | (brows == hrows ? 0u : 0x80000000u);
             }
-          } else if (r < rend && x == xb - 1) {  // upper part of a segment cut at xb
+          } else if ((kRangeEnd ? lrow >= HS : r < rend) && x == xb - 1) {  // upper part of a segment cut at xb
+            RQA_DCHECK(r < R - 1 && ((int64_t)unit.idx * (R - 1) + r) * D + delta < ua.cap_drec);
             ua.drec[((int64_t)unit.idx * (R - 1) + r) * D + delta].x =
                 diag_piece_end(st[r], true, LineSink{&hist, 0u});
           }
@@ -1028,6 +1049,7 @@ unit_kernel(const UnitArgs ua, const int W_rt) {
     if (lr < hrows) {
       const uint2 rsv = rowst[lr];
       const Seg sg = runs_finish(RunState{rsv.x, rsv.y});
+      RQA_DCHECK((int64_t)unit.idx * H + lr < ua.cap_piece);
       piece[lr] = make_uint2(sg.first, sg.last);
     }
   }

@@ -1,5 +1,6 @@
 #!/bin/bash
 # compute-sanitizer evidence: memcheck, racecheck, synccheck, initcheck over scripts/sanitize_cases.py
+# (kept for reference: the GPU pool has since closed compute-sanitizer; use gpu_checked.sh)
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 export RQA_PREFILTER=${RQA_PREFILTER:-1}
 # empty the shared bins every 2 iterations: exercises the mid-unit flush path
