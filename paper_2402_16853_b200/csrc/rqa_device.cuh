@@ -13,27 +13,33 @@
 // Checked builds (make EXTRA=-DRQA_CHECKS, scripts/gpu_checked.sh): device
 // bounds / capacity assertions on every global write of the band kernel and
 // the diagonal-piece join, the histogram indices, and the event-ring and
-// candidate-list occupancies.  A failed check prints its condition and traps
-// (the C-ABI call then fails).  Compiled out by default.
-#if defined(RQA_CHECKS) && defined(RQA_CHECKS_TRAP_ONLY)
-#define RQA_DCHECK(cond) \
-  do {                   \
-    if (!(cond)) __trap(); \
-  } while (0)
-#elif defined(RQA_CHECKS)
-#define RQA_DCHECK(cond)                                                          \
-  do {                                                                           \
-    if (!(cond)) {                                                               \
-      printf("RQA_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
-             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                         \
-      __trap();                                                                  \
-    }                                                                            \
+// candidate-list occupancies.  A failed check traps (the C-ABI call then
+// fails with a launch error).  Compiled out by default (the default build's
+// SASS is unchanged).  RQA_CHECKS_PRINTF: bit mask of check sites that also
+// print their condition (1 Hist/GHist, 2 hist_red, 4 event ring, 8 band-kernel
+// writes, 16 piece join).  Known issue: a printf in hist_red (site 2, inside
+// the out-of-line event drain) changed results although no check fired; the
+// trap-only build and the other sites are parity-green.  Not resolved (no
+// compute-sanitizer on this pool), so the checked build does not print.
+#ifndef RQA_CHECKS_PRINTF
+#define RQA_CHECKS_PRINTF 0
+#endif
+#ifdef RQA_CHECKS
+#define RQA_DCHECK_AT(site, cond)                                                     \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      if ((RQA_CHECKS_PRINTF) & (site))                                               \
+        printf("RQA_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+               __LINE__, (int)blockIdx.x, (int)threadIdx.x);                          \
+      __trap();                                                                       \
+    }                                                                                 \
   } while (0)
 #else
-#define RQA_DCHECK(cond) \
-  do {                   \
+#define RQA_DCHECK_AT(site, cond) \
+  do {                            \
   } while (0)
 #endif
+#define RQA_DCHECK(cond) RQA_DCHECK_AT(8, cond)
 
 namespace rqa {
 
@@ -90,7 +96,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // pin the surrounding loads and stores.
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
 
@@ -113,7 +119,7 @@ struct Hist {
       const uint32_t addr = sh + 4u * (uint32_t)(kind * kSmemBins + (int)len);
       asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
     } else {
-      RQA_DCHECK(len >= 0 && len < stride && kind >= 0 && kind < 3);
+      RQA_DCHECK_AT(1, len >= 0 && len < stride && kind >= 0 && kind < 3);
       atomicAdd(&g[kind * stride + len], (unsigned long long)w);
     }
   }
@@ -124,7 +130,7 @@ struct GHist {
   unsigned long long* g;
   int64_t stride;
   __device__ __forceinline__ void add(int kind, int64_t len, uint32_t w) const {
-    RQA_DCHECK(len >= 0 && len < stride && kind >= 0 && kind < 3);
+    RQA_DCHECK_AT(1, len >= 0 && len < stride && kind >= 0 && kind < 3);
     atomicAdd(&g[kind * stride + len], (unsigned long long)w);
   }
 };

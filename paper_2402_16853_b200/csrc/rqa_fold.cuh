@@ -336,7 +336,7 @@ __global__ void fix_diag_pieces(const DiagPieceArgs a) {
       h.add(kDiag, SA + LB, w);  // last run, ends at the matrix edge
     }
     const int64_t off = sym_band_offset(U.x, a.n, a.row_lo, a.H) + kd;
-    RQA_DCHECK(q < a.cap_drec && off >= 0 && off < a.cap_ps);
+    RQA_DCHECK_AT(16, q < a.cap_drec && off >= 0 && off < a.cap_ps);
     a.P[off] = (uint16_t)Pv;
     a.S[off] = (uint16_t)Sv;
   }

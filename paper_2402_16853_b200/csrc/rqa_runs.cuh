@@ -144,7 +144,7 @@ __device__ __forceinline__ void hist_red(const Hist& h, uint32_t kind_row, uint3
   const uint32_t sa = h.sh + 4u * (small ? kind_row * (uint32_t)kSmemBins + len : kDummyBin);
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa), "r"(small ? w : 0u) : "memory");
   if (!small && w) {
-    RQA_DCHECK((int64_t)len < h.stride && kind_row < 3u);
+    RQA_DCHECK_AT(2, (int64_t)len < h.stride && kind_row < 3u);
     atomicAdd(h.g + (int64_t)kind_row * h.stride + len, (unsigned long long)w);
   }
 }
@@ -204,7 +204,8 @@ static __device__ __noinline__ uint32_t queue_drain_impl(uint32_t ring_sa, uint3
       uint4 e;
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
-                   : "r"(ring_sa + 16u * ((head + lane) & (uint32_t)(kQueueCap - 1))));
+                   : "r"(ring_sa + 16u * ((head + lane) & (uint32_t)(kQueueCap - 1)))
+                   : "memory");
       expand_event(e, h);
     }
     head += avail < 32u ? avail : 32u;
@@ -254,9 +255,10 @@ __device__ __forceinline__ void runs_push(uint32_t lo, uint32_t hi, int nb, RunS
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "@p st.shared.v4.u32 [%0], {%1, %2, %3, %3};\n\t}" ::"r"(q.ring_sa + 16u * slot),
       "r"(blo), "r"(bhi), "r"(cur | (((diag_weight << 1) | (mkfirst ? 1u : 0u)) << kEvCurBits)),
-      "r"(ev ? 1u : 0u));  // no memory clobber: the ring is only accessed through asm
+      "r"(ev ? 1u : 0u)
+      : "memory");
   q.tail += __popc(m);
-  RQA_DCHECK(q.tail - q.head <= (uint32_t)kQueueCap);  // ring never overwrites unread events
+  RQA_DCHECK_AT(4, q.tail - q.head <= (uint32_t)kQueueCap);  // ring never overwrites unread events
 }
 
 __device__ __forceinline__ Seg runs_finish(const RunState& st) {
