@@ -22,6 +22,13 @@
 namespace rqa {
 namespace {
 
+// Runtime knob: the variable's value, or nullptr when it is unset or empty
+// (an empty RQA_WAVES= or RQA_PREFILTER= means "default", not 0).
+const char* env_knob(const char* name) {
+  const char* v = getenv(name);
+  return (v && v[0]) ? v : nullptr;
+}
+
 // NVTX range over a host-side phase (header-only NVTX 3: free without a
 // profiler attached; nsys / ncu --nvtx show the phases of every call).
 struct NvtxRange {
@@ -433,7 +440,7 @@ bool prefilter_f32_bound(double dstar, double maxabs, float* d2) {
 // width condition (tests).  Results are bit-identical on every path.
 int plan_precision(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
   p->filt = -1;
-  static const char* fenv = getenv("RQA_FILTER");
+  static const char* fenv = env_knob("RQA_FILTER");
   const int want = fenv ? atoi(fenv) : 0;
   Variant fv;
   const bool packed = find_variant_f32(p->metric, p->m, p->tau, true, &fv);
@@ -478,7 +485,7 @@ inline double prefilter_max(int m) { return 0.05 * std::max(1.0, m / 3.0); }
 int plan_prefilter(Workspace* ws, Problem* p, cudaStream_t st, char* err, size_t errlen) {
   NvtxRange nvtx_("rqa.plan_prefilter");
   if (p->precision != 64 || p->filt != -1) return RQA_OK;
-  static const char* penv = getenv("RQA_PREFILTER");
+  static const char* penv = env_knob("RQA_PREFILTER");
   const int want = penv ? atoi(penv) : 2;
   if (want == 0) return RQA_OK;
   Variant pv;
@@ -557,7 +564,7 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   // (round 2): 32 waves for a whole 2^20 run (~7,100 iterations per resident
   // CTA), 16 for one of 8 stripes of it (~890): waves = 16 (T / 887)^(1/3),
   // T = iterations per resident CTA, clamped to [8, 64]; RQA_WAVES overrides
-  static const char* wenv = getenv("RQA_WAVES");
+  static const char* wenv = env_knob("RQA_WAVES");
   const double per_slot = (double)total / std::max(1, slots);
   const int64_t waves = wenv ? std::max(1, atoi(wenv))
                              : std::min<int64_t>(64, std::max<int64_t>(
@@ -565,7 +572,7 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   // units of >= 16 iterations keep the recomputed iteration <= 1/16 of the
   // work, unless the whole triangle is too small to fill the GPU once (C1):
   // then parallelism wins over the recomputation
-  static const char* menv = getenv("RQA_MIN_UNIT");
+  static const char* menv = env_knob("RQA_MIN_UNIT");
   const int64_t min_len = menv ? std::max(1, atoi(menv))
                                : std::min<int64_t>(16, std::max<int64_t>(1, total / slots));
   int64_t len = std::max<int64_t>(min_len, total / std::max<int64_t>(1, waves * slots));
@@ -575,7 +582,7 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   // the unit count (boundary recomputation) stays about the same.  Sweep
   // 0 / 0.25 / 0.35 / 0.5: 0.25 best (C3 -0.3 %, P -0.7 %, C4 -1.1 %, one of 8
   // C3 stripes -1 %)
-  static const char* tenv = getenv("RQA_TAIL_FRAC");
+  static const char* tenv = env_knob("RQA_TAIL_FRAC");
   const double tf = tenv ? std::min(0.9, std::max(0.0, atof(tenv))) : 0.25;
   UnitPlan pl;
   pl.band_start.assign(nb + 1, 0);
@@ -684,9 +691,9 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   a.rowlead = nullptr;
   a.hist = hist;
   a.points = points;
-  static const char* skip_env = getenv("RQA_SKIP");  // profiling only: skip phases
+  static const char* skip_env = env_knob("RQA_SKIP");  // profiling only: skip phases
   a.skip = skip_env ? atoi(skip_env) : 0;
-  static const char* flush_env = getenv("RQA_FLUSH_EVERY");  // tests: power of two
+  static const char* flush_env = env_knob("RQA_FLUSH_EVERY");  // tests: power of two
   const int flush_every = flush_env ? std::max(1, atoi(flush_env)) : 4096;
   a.flush_mask = ((flush_every & (flush_every - 1)) == 0 ? flush_every : 4096) - 1;
   a.timers = nullptr;
@@ -767,7 +774,7 @@ int launch_rows(Workspace* ws, const Problem& p, int64_t row_lo, int64_t row_hi,
   h.out_row = reinterpret_cast<uint2*>(rowpart);
   // one launch: the diagonal fold (about a fifth of the fold time) and the
   // hook fold share the grid
-  static const char* dfrac = getenv("RQA_FOLD_DIAG_SHARE");
+  static const char* dfrac = env_knob("RQA_FOLD_DIAG_SHARE");
   const double share = dfrac ? atof(dfrac) : 0.3;
   const int dblocks = (int)std::max<int64_t>(1, (int64_t)(blocks * share));
   unit_fold_all<<<(int)blocks + dblocks, threads, 0, st>>>(f, h, mode, dblocks);

@@ -78,3 +78,32 @@ def test_plan_rejects_bad_arguments():
     assert lib.rqa_plan_units(100, 50, 20, 256, 4, 296, None, 0, ctypes.byref(c)) != 0
     assert lib.rqa_plan_units(100, 0, 100, 100, 4, 296, None, 0, ctypes.byref(c)) != 0
     assert lib.rqa_plan_units(100, 0, 100, 256, 4, 0, None, 0, ctypes.byref(c)) != 0
+
+
+def _unit_count_in_subprocess(env_extra):
+    """Unit count of the full 2^20 plan in a fresh process (knobs are read once)."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import ctypes, sys; sys.path.insert(0, '.');"
+            "from paper_2402_16853_b200 import _native; lib = _native.lib();"
+            "c = ctypes.c_int64();"
+            "assert lib.rqa_plan_units(1 << 20, 0, 1 << 20, 256, 4, 296, None, 0, ctypes.byref(c)) == 0;"
+            "print(c.value)")
+    env = dict(os.environ)
+    for k in ("RQA_WAVES", "RQA_TAIL_FRAC", "RQA_MIN_UNIT"):
+        env.pop(k, None)
+    env.update(env_extra)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, check=True)
+    return int(out.stdout.strip())
+
+
+def test_empty_knobs_mean_default():
+    # RQA_WAVES= (empty) used to parse as 0 -> one wave: a 2 % slower plan
+    base = _unit_count_in_subprocess({})
+    assert _unit_count_in_subprocess({"RQA_WAVES": "", "RQA_TAIL_FRAC": "",
+                                      "RQA_MIN_UNIT": ""}) == base
+    assert _unit_count_in_subprocess({"RQA_WAVES": "8"}) < base
