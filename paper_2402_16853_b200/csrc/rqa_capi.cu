@@ -576,14 +576,15 @@ UnitPlan plan_units(const Problem& p, int64_t row_lo, int64_t row_hi, int slots)
   const int64_t min_len = menv ? std::max(1, atoi(menv))
                                : std::min<int64_t>(16, std::max<int64_t>(1, total / slots));
   int64_t len = std::max<int64_t>(min_len, total / std::max<int64_t>(1, waves * slots));
-  // tail fraction (RQA_TAIL_FRAC, default 0.25): the last tf of every band's
+  // tail fraction (RQA_TAIL_FRAC, default 0.15): the last tf of every band's
   // sweep is cut into units of len/2 and the rest into units of 2 len, so the
   // longest-first launch order ends with small units (shorter tail) while
   // the unit count (boundary recomputation) stays about the same.  Sweep
   // 0 / 0.25 / 0.35 / 0.5: 0.25 best (C3 -0.3 %, P -0.7 %, C4 -1.1 %, one of 8
-  // C3 stripes -1 %)
+  // C3 stripes -1 % against 0); then 0.15 / 0.2 / 0.25 with the range-tested
+  // kernels: 0.15 (C3 -0.12 %, C4 -0.24 %, C5 -0.05 %, P and stripes equal)
   static const char* tenv = env_knob("RQA_TAIL_FRAC");
-  const double tf = tenv ? std::min(0.9, std::max(0.0, atof(tenv))) : 0.25;
+  const double tf = tenv ? std::min(0.9, std::max(0.0, atof(tenv))) : 0.15;
   UnitPlan pl;
   pl.band_start.assign(nb + 1, 0);
   auto cut = [&](int64_t b, int64_t lo, int64_t hi, int64_t piece) {
